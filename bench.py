@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark: NU points/sec (exec, device-timed) for the BASELINE configs.
+
+Default workload = BASELINE.json configs[1] ("C2"): 2D type-2 single
+precision, N = 1024 x 1024 (fine 2048 x 2048), M = 1e7 uniform points,
+eps = 1e-5.  A step = one execute() (pad -> cuFFT inverse -> interp) with
+the points already set (the paper's "exec").
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c2] [--method sm]
+  python bench.py --impl reference ...   # the reference algorithm on host cores
+
+Multi-GPU (torchrun, one process per GPU, NCCL): type-2 configs shard the
+points (each rank owns its own M points, weak scaling) against a replicated
+fine grid; rank 0's modes are broadcast every step (the real exchange).
+Type-1 configs shard points and sum the per-rank fine grids with an NCCL
+reduce before the root's FFT + deconvolution.  c5 runs independent
+replicas (no collective).  Times are CUDA-event device times, max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(type=1, modes=(256, 256), M=1_000_000, dist="rand", eps=1e-5, prec="single",
+               desc="C1 2D type-1 f32 N=256^2 M=1e6 uniform eps=1e-5"),
+    "c2": dict(type=2, modes=(1024, 1024), M=10_000_000, dist="rand", eps=1e-5, prec="single",
+               desc="C2 2D type-2 f32 N=1024^2 M=1e7 uniform eps=1e-5"),
+    "c3a": dict(type=1, modes=(128, 128, 128), M=10_000_000, dist="cluster", eps=1e-6,
+                prec="single", desc="C3a 3D type-1 f32 N=128^3 M=1e7 box-cluster eps=1e-6"),
+    "c3b": dict(type=1, modes=(128, 128, 128), M=10_000_000, dist="gauss", eps=1e-6,
+                prec="single",
+                desc="C3b 3D type-1 f32 N=128^3 M=1e7 Gaussian(0,(pi/8)^2) eps=1e-6"),
+    "c4t1": dict(type=1, modes=(256, 256, 256), M=100_000_000, dist="rand", eps=1e-12,
+                 prec="double", desc="C4 3D type-1 f64 N=256^3 M=1e8 uniform eps=1e-12"),
+    "c4t2": dict(type=2, modes=(256, 256, 256), M=100_000_000, dist="rand", eps=1e-12,
+                 prec="double", desc="C4 3D type-2 f64 N=256^3 M=1e8 uniform eps=1e-12"),
+    "c5": dict(type=12, modes=(128, 128, 128), M=10_000_000, dist="rand", eps=1e-12,
+               prec="double",
+               desc="C5 3D type-2 then type-1 f64 N=128^3 M=1e7 per rank, eps=1e-12"),
+}
+METRIC = "NU points/sec (exec, device-timed) at tol eps, 2D/3D type 1/2, at 1/2/4/8 B200"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            j = json.load(fh)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def algorithmic_bytes(cfg, fine):
+    """SURVEY.md §8(d) per-kernel bytes of the dominant kernel
+    (spread for type 1, interp for type 2): M (d+2) s + 2 n_tot s."""
+    d = len(cfg["modes"])
+    s = 4 if cfg["prec"] == "single" else 8
+    return cfg["M"] * (d + 2) * s + 2 * int(np.prod(fine)) * s
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+                 "utilization.gpu", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons, util = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+                util.append(float(parts[8]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        busy = [s for s, u in zip(sm, util) if u > 0] or sm
+        return {"sm_mhz": float(np.median(busy)) if busy else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_inputs(cfg, seed, rank=0):
+    from oracle import oracle as orc   # generators only (seeded synthetic data)
+    grid = orc.make_grid(cfg["modes"], cfg["eps"], cfg["prec"])
+    rdt = np.float32 if cfg["prec"] == "single" else np.float64
+    cdt = np.complex64 if cfg["prec"] == "single" else np.complex128
+    pts = orc.gen_points(cfg["dist"], cfg["M"], grid, seed + rank, rdt)
+    rng = np.random.default_rng(seed + 17)
+    nmodes = int(np.prod(cfg["modes"]))
+    f = (rng.uniform(0, 1, nmodes) + 1j * rng.uniform(0, 1, nmodes)).astype(cdt)
+    c = (rng.uniform(0, 1, cfg["M"]) + 1j * rng.uniform(0, 1, cfg["M"])).astype(cdt)
+    return grid, pts, f.reshape(cfg["modes"][::-1]), c
+
+
+# ---------------------------------------------------------------- reference
+
+def cpu_reference(cfg, steps, warmup, sample_cap):
+    """The reference algorithm (oracle C port of nufftkit, all host threads)
+    on a bounded sample: fixed-size stages (pad/deconv, FFT) at full size,
+    the M-proportional stage (interp / spread) on `sample` points and scaled
+    linearly to M.  Returns (pts_per_sec, cores, sample description)."""
+    from oracle import oracle as orc
+    threads = orc.host_threads()
+    sub = dict(cfg)
+    sample = min(cfg["M"], sample_cap)
+    sub["M"] = sample
+    grid, pts, f, c = make_inputs(sub, 0)
+    types = [2, 1] if cfg["type"] == 12 else [cfg["type"]]
+    plans = {}
+    for t in types:
+        p = orc.OraclePlan(t, cfg["modes"], cfg["eps"], "sm" if t == 1 else "gmsort",
+                           cfg["prec"], workers=threads)
+        p.set_points(pts)
+        plans[t] = p
+    times = []
+    for it in range(warmup + steps):
+        tot = 0.0
+        for t in types:
+            p = plans[t]
+            g, prm = p.grid, p.params
+            if t == 2:
+                t0 = time.perf_counter()
+                bh = orc.deconvolve_type2(f, g, prm, p.corr)
+                b = orc.fft_fine(bh, "inverse", threads).astype(prm.complex_dtype, copy=False)
+                t1 = time.perf_counter()
+                orc.interpolate(p.points, b, prm, g, p.layout, threads)
+                t2 = time.perf_counter()
+                fixed, prop = t1 - t0, t2 - t1
+            else:
+                t0 = time.perf_counter()
+                b = p.spread(c)
+                t1 = time.perf_counter()
+                bh = orc.fft_fine(b, "forward", threads).astype(prm.complex_dtype, copy=False)
+                orc.deconvolve_type1(bh, g, prm, p.corr)
+                t2 = time.perf_counter()
+                fixed, prop = t2 - t1, t1 - t0
+            tot += fixed + prop * (cfg["M"] / sample)
+        if it >= warmup:
+            times.append(tot)
+    t_step = float(np.median(times))
+    npts = cfg["M"] * len(types)
+    desc = (f"oracle C port (nufftkit algorithm: {'GM-sort interp' if 2 in types else ''}"
+            f"{' + ' if len(types) == 2 else ''}{'SM spread' if 1 in types else ''}, "
+            f"scipy.fft) on {threads} host threads; M-proportional stage timed on "
+            f"{sample} of {cfg['M']} points and scaled; pad/FFT/deconv at full size; "
+            f"median of {steps}")
+    return npts / t_step, threads, desc, t_step
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    v, cores, desc, t_step = cpu_reference(cfg, args.steps, args.warmup, args.cpu_sample)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "NU pts/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if cfg["prec"] == "single" else "f64",
+            "data": "synthetic (seeded numpy: uniform / cluster / gauss points, U[0,1)^2 "
+                    "complex strengths)",
+            "config": {"workload": cfg["desc"]},
+            "cpu_baseline": {"value": v, "unit": "NU pts/s", "cores": cores, "kind": "port",
+                             "sample": desc},
+            "e2e": {"value": v, "unit": "NU pts/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- ours
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2102_08463_b200 as nk
+
+    grid, pts, f_host, c_host = make_inputs(cfg, args.seed, rank)
+    types = [2, 1] if cfg["type"] == 12 else [cfg["type"]]
+    plans = {}
+    for t in types:
+        method = args.method or "default"
+        plans[t] = nk.make_plan(t, cfg["modes"], cfg["eps"], method, cfg["prec"], timing=True)
+        plans[t].set_points(torch.from_numpy(pts).to(dev))
+    torch.cuda.synchronize()
+    f_dev = torch.from_numpy(f_host).to(dev)
+    c_dev = torch.from_numpy(c_host).to(dev)
+    out_t2 = torch.empty(cfg["M"], dtype=c_dev.dtype, device=dev)
+    out_t1 = torch.empty(cfg["modes"][::-1], dtype=c_dev.dtype, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    shard_t1 = world > 1 and cfg["type"] == 1
+    fine_buf = None
+    if shard_t1:
+        fine_buf = torch.empty(plans[1].grid.fine_shape, dtype=c_dev.dtype, device=dev)
+
+    from paper_2102_08463_b200 import _lib
+
+    def step():
+        launches = 0
+        for t in types:
+            p = plans[t]
+            if t == 2:
+                if world > 1 and cfg["type"] == 2:
+                    dist.broadcast(f_dev, 0)
+                p.execute(f_dev, out_t2)
+            elif shard_t1:
+                # per-rank spread -> NCCL reduce of the fine grid -> root FFT + deconv
+                _lib.check(p._lib.nk_spread(p._h, c_dev.data_ptr(), fine_buf.data_ptr()))
+                launches += 1
+                dist.reduce(fine_buf, 0)
+                if rank == 0:
+                    _lib.check(p._lib.nk_fft(p._h, fine_buf.data_ptr(), -1))
+                    _lib.check(p._lib.nk_deconv_type1(p._h, fine_buf.data_ptr(),
+                                                      out_t1.data_ptr()))
+                    launches += 1
+                continue
+            else:
+                p.execute(c_dev, out_t1)
+            launches += p.last_launch_count()
+        return launches
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    step_ms, dom_ms, launches = [], [], 0
+    dom_type = types[0]
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)                       # L2 flush between timed steps
+            torch.cuda.synchronize()
+            start.record()
+            launches += step()
+            end.record()
+            torch.cuda.synchronize()
+            step_ms.append(start.elapsed_time(end))
+            if not shard_t1:
+                st = plans[dom_type].stage_times()
+                dom_ms.append(st["interp" if dom_type == 2 else "spread"])
+    tot_ms = float(np.sum(step_ms))
+    dom_avg = float(np.mean(dom_ms)) if dom_ms else None
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+
+    # ---- e2e: the public API with pinned host buffers, copies inside the timing
+    e2e = None
+    if not shard_t1:
+        pin_in = {}
+        for t in types:
+            src = f_host if t == 2 else c_host
+            b = torch.empty(src.shape, dtype=c_dev.dtype, pin_memory=True)
+            b.numpy()[...] = src
+            pin_in[t] = b.numpy()
+        pin_out = {2: torch.empty(cfg["M"], dtype=c_dev.dtype, pin_memory=True).numpy(),
+                   1: torch.empty(cfg["modes"][::-1], dtype=c_dev.dtype,
+                                  pin_memory=True).numpy()}
+        for _ in range(max(1, args.warmup)):
+            for t in types:
+                plans[t].execute(pin_in[t], pin_out[t])
+        e2e_s = []
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for t in types:
+                plans[t].execute(pin_in[t], pin_out[t])    # H2D + exec + D2H, synchronous
+            e2e_s.append(time.perf_counter() - t0)
+        e2e_t = float(np.sum(e2e_s))
+        if world > 1:
+            t = torch.tensor([e2e_t], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_t = float(t.item())
+        csz = c_dev.element_size()
+        h2d = sum((int(np.prod(cfg["modes"])) if t == 2 else cfg["M"]) * csz for t in types)
+        d2h = sum((cfg["M"] if t == 2 else int(np.prod(cfg["modes"]))) * csz for t in types)
+        e2e = {"value": world * cfg["M"] * len(types) * args.steps / e2e_t, "unit": "NU pts/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    if rank == 0:
+        fine = plans[dom_type].grid.fine
+        peak, peak_src = peaks()
+        line = {
+            "metric": METRIC,
+            "value": world * cfg["M"] * len(types) * args.steps / (tot_ms / 1e3),
+            "unit": "NU pts/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if cfg["prec"] == "single" else "f64",
+            "data": "synthetic (seeded numpy: uniform / cluster / gauss points, U[0,1)^2 "
+                    "complex strengths), inputs resident in HBM",
+            "config": {"workload": cfg["desc"], "method": plans[dom_type].method,
+                       "fine": list(fine), "w": plans[dom_type].params.w,
+                       "bin_dims": list(plans[dom_type].bin_dims),
+                       "l2": "flushed between timed steps (256 MiB write)",
+                       "parallelism": f"points sharded over {world} GPU(s)"
+                                      if world > 1 else "1 GPU"},
+            "gpu_launches": launches,
+        }
+        if dom_avg:
+            B = algorithmic_bytes(cfg, fine)
+            ach = B / (dom_avg / 1e3) / 1e9
+            line["roofline"] = {"bound": "hbm", "kernel": "interp" if dom_type == 2 else "spread",
+                                "achieved": ach, "peak": peak, "unit": "GB/s",
+                                "frac": ach / peak, "traffic": traffic_for(args.config),
+                                "algorithmic_bytes": B, "kernel_ms": dom_avg,
+                                "peak_source": peak_src}
+            line["stage_ms"] = plans[dom_type].stage_times()
+        if e2e:
+            line["e2e"] = e2e
+        line["clocks"] = clk.summary()
+        if world == 1 and not args.no_cpu_baseline:
+            v, cores, desc, _ = cpu_reference(cfg, 2, 1, args.cpu_sample)
+            line["cpu_baseline"] = {"value": v, "unit": "NU pts/s", "cores": cores,
+                                    "kind": "port", "sample": desc}
+        print(json.dumps(line), flush=True)
+    for p in plans.values():
+        p.destroy()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def traffic_for(config):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(config)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--method", default=None)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-sample", type=int, default=2_000_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,83 @@
+// Device helpers: the exact FP64 fold, the ES kernel, complex atomics.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "nk_internal.cuh"
+
+// binsort.py:98-100 grid_coords with numpy remainder semantics, bit-exact:
+// r = fmod(x + pi, 2 pi); r < 0 -> r + 2 pi; r == 0 -> +0.0; v = r * (n / 2 pi).
+// Explicit _rn intrinsics keep nvcc from contracting into FMAs.
+__device__ __forceinline__ double nk_fold(double x, double scale) {
+    double a = __dadd_rn(x, NK_PI);
+    double r = fmod(a, NK_TWO_PI);
+    if (r != 0.0) {
+        if (r < 0.0) r = __dadd_rn(r, NK_TWO_PI);
+    } else {
+        r = 0.0;
+    }
+    return __dmul_rn(r, scale);
+}
+
+// binsort.py:126-128: cell = clamp(floor(v), 0, n-1).  v is finite here.
+__device__ __forceinline__ int nk_cell(double v, int n) {
+    double f = floor(v);
+    int c = f >= (double)(n - 1) ? n - 1 : (int)f;
+    return c < 0 ? 0 : c;
+}
+
+// ES kernel exp(beta (sqrt(1 - z^2) - 1)) on |z| <= 1 (_kernels.py:20-26).
+// Single precision uses exp2 with beta*log2(e) folded in (one MUFU.EX2);
+// double uses the accurate libdevice exp.
+__device__ __forceinline__ float nk_es(float z, const Geom &g) {
+    float t = 1.0f - z * z;
+    return t >= 0.0f ? exp2f(g.betaf_log2e * (sqrtf(t) - 1.0f)) : 0.0f;
+}
+__device__ __forceinline__ double nk_es(double z, const Geom &g) {
+    double t = 1.0 - z * z;
+    return t >= 0.0 ? exp(g.beta * (sqrt(t) - 1.0)) : 0.0;
+}
+
+template <typename T> __device__ __forceinline__ T nk_ceil(T x);
+template <> __device__ __forceinline__ float nk_ceil<float>(float x) { return ceilf(x); }
+template <> __device__ __forceinline__ double nk_ceil<double>(double x) { return ceil(x); }
+
+// Kernel row for one axis: local coordinate u (relative to the bin corner),
+// returns the local start cell ceil(u - w/2) (_kernels.py:43-46) and fills
+// ker[r] = phi((start + r - u) * 2/w) (_kernels.py:29-33).
+template <typename T, int W>
+__device__ __forceinline__ int nk_kernel_row(T u, const Geom &g, T *ker) {
+    T st = nk_ceil<T>(u - (T)(0.5 * W));
+#pragma unroll
+    for (int r = 0; r < W; ++r) ker[r] = nk_es((st + (T)r - u) * (T)(2.0 / W), g);
+    return (int)st;
+}
+
+__device__ __forceinline__ int nk_wrap(int l, int n) {
+    l = l < 0 ? l + n : l;
+    return l >= n ? l - n : l;
+}
+
+// Complex accumulation into global memory: native REDG.E.ADD.F32x2 / F64.
+__device__ __forceinline__ void nk_red(float2 *p, float re, float im) {
+    atomicAdd(p, make_float2(re, im));
+}
+__device__ __forceinline__ void nk_red(double2 *p, double re, double im) {
+    atomicAdd(&p->x, re);
+    atomicAdd(&p->y, im);
+}
+
+// Decode a bin key into its corner cells (axis 1 fastest, binsort.py:103-111).
+__device__ __forceinline__ void nk_bin_corner(int key, const Geom &g, int *corner) {
+    int b0 = key % g.nb[0];
+    int r = key / g.nb[0];
+    corner[0] = b0 * g.m[0];
+    if (g.dim == 2) {
+        corner[1] = r * g.m[1];
+        corner[2] = 0;
+    } else {
+        corner[1] = (r % g.nb[1]) * g.m[1];
+        corner[2] = (r / g.nb[1]) * g.m[2];
+    }
+}

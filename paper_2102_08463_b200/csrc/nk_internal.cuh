@@ -1,0 +1,123 @@
+// Internal declarations shared by the libnufft_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/nufft_b200.h"
+
+#define NK_PI 3.141592653589793
+#define NK_TWO_PI (2.0 * NK_PI)
+
+// ---------------------------------------------------------------- errors
+void nk_set_error(const std::string &msg);
+void nk_set_error_index(int64_t idx);
+
+#define NK_CUDA(expr)                                                                 \
+    do {                                                                              \
+        cudaError_t _e = (expr);                                                      \
+        if (_e != cudaSuccess) {                                                      \
+            nk_set_error(std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " + \
+                         __FILE__ + ":" + std::to_string(__LINE__));                  \
+            return _e == cudaErrorMemoryAllocation ? NK_ERR_MEMORY : NK_ERR_CUDA;     \
+        }                                                                             \
+    } while (0)
+
+#define NK_LAUNCH_CHECK() NK_CUDA(cudaGetLastError())
+
+// -------------------------------------------------------------- geometry
+// Per-plan geometry passed by value to kernels.  Axis 0 is the reference's
+// axis 1 (fastest).
+struct Geom {
+    int dim;
+    int n[3];       // fine sizes
+    int N[3];       // mode counts
+    int m[3];       // bin dims
+    int nb[3];      // bins per axis
+    int halo;       // ceil(w/2)
+    int w;
+    double scale[3];  // n_i / (2 pi), binsort.py:99
+    float betaf, betaf_log2e;
+    double beta;
+};
+
+template <typename T> struct cplx;
+template <> struct cplx<float> { typedef float2 t; };
+template <> struct cplx<double> { typedef double2 t; };
+
+// -------------------------------------------------------------- plan
+struct nk_plan {
+    int type, dim, prec, method;
+    int64_t N[3], n[3];
+    double eps;
+    int w;
+    double beta;
+    double alpha[3];
+    int eps_clamped;
+    int bin_dims[3];
+    int64_t nb[3];
+    int64_t nbins;
+    int msub;
+    int halo;
+    int device;
+    cudaStream_t stream;
+    int timing;
+    Geom geom;
+
+    int64_t n_tot, N_tot;
+    size_t csize;   // bytes per complex element
+    void *d_fine;   // fine grid (n_tot complex)
+    void *d_corr;   // per-axis correction factors incl. (2/w) and (-1)^k (plan precision)
+    cufftHandle fft;
+    bool fft_ok;
+
+    // points
+    int64_t M;
+    bool have_points;
+    int64_t cap_M;
+    int32_t *d_keys_in;     // bin key per input point
+    int32_t *d_keys;        // bin key in visit order (sorted, or input order for GM)
+    int32_t *d_perm;        // visit position -> input index (NULL semantics for GM)
+    int32_t *d_counts;      // nbins
+    int32_t *d_starts;      // nbins + 1
+    void *d_pts;            // dim arrays of cap_M local coords (plan precision)
+    int32_t *d_alt_keys, *d_alt_vals;  // radix scratch
+    int32_t *d_tile_hist;
+    int64_t cap_tile_hist;
+    int32_t *d_scan_tmp;
+    int64_t cap_scan_tmp;
+    unsigned long long *d_bad;
+    bool sorted;
+
+    // subproblems
+    int64_t S, cap_S;
+    int32_t *d_nsub_off;    // nbins + 1
+    int32_t *d_sub_bin, *d_sub_start, *d_sub_stop;
+    int max_sub_smem;       // bytes
+
+    // staging for host pointers
+    void *d_in_stage, *d_out_stage;
+    size_t cap_in_stage, cap_out_stage;
+
+    // timing
+    cudaEvent_t ev[4];
+    bool ev_ok;
+    int last_launches;
+};
+
+// -------------------------------------------------------------- launchers
+int nk_scan_exclusive(nk_plan *p, const int32_t *in, int32_t *out, int64_t n);
+int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y,
+                   const void *z, int64_t stride);
+int nk_launch_spread(nk_plan *p, const void *c, void *fine, int *launches);
+int nk_launch_interp(nk_plan *p, const void *fine, void *out, int *launches);
+int nk_launch_deconv1(nk_plan *p, const void *spec, void *modes);
+int nk_launch_deconv2(nk_plan *p, const void *modes, void *spec);
+int nk_export_subproblems(const nk_plan *p, int32_t *bin_ids, int32_t *starts,
+                          int32_t *stops, int32_t *offsets, int32_t *padded);
+
+// plan-time host math (nk_host.cpp)
+void nk_kernel_fourier_host(double beta, const double *xi, int64_t n, double *out);

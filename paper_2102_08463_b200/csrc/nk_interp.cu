@@ -1,0 +1,200 @@
+// Type-2 step 3: ES-kernel interpolation (the adjoint gather).
+//
+//  K7  GM / GM-sort (_kernels.py:150-198; wrapper SPEC.md:358-366): one
+//      thread per point in input / bin-sorted order gathers its w^d
+//      footprint from the fine grid and writes slot perm[j] (output keeps
+//      the input indexing).
+//  K7s staged ("sm" for type 2): one CTA per subproblem copies its padded
+//      bin (with periodic wrap) from HBM into shared memory once, then its
+//      points gather from shared memory.  Same per-point arithmetic.
+#include "nk_device.cuh"
+
+namespace {
+
+template <typename T, int D, int W>
+__device__ __forceinline__ typename cplx<T>::t
+gather_global(const typename cplx<T>::t *__restrict__ fine, const Geom &g, int s1, int s2,
+              int s3, const T *k1, const T *k2, T u3, T st3) {
+    typedef typename cplx<T>::t C;
+    const int n1 = g.n[0], n2 = g.n[1], n3 = g.n[2];
+    int l1[W];
+#pragma unroll
+    for (int a = 0; a < W; ++a) l1[a] = nk_wrap(s1 + a, n1);
+    T accr = 0, acci = 0;
+#pragma unroll 1
+    for (int e = 0; e < (D == 3 ? W : 1); ++e) {
+        int64_t plane = D == 3 ? (int64_t)nk_wrap(s3 + e, n3) * n2 : 0;
+        T mr = 0, mi = 0;
+#pragma unroll
+        for (int b = 0; b < W; ++b) {
+            const C *row = fine + (plane + nk_wrap(s2 + b, n2)) * (int64_t)n1;
+            T ir = 0, ii = 0;
+#pragma unroll
+            for (int a = 0; a < W; ++a) {
+                C v = __ldg(row + l1[a]);
+                ir += v.x * k1[a];
+                ii += v.y * k1[a];
+            }
+            mr += ir * k2[b];
+            mi += ii * k2[b];
+        }
+        if (D == 3) {
+            const T k3 = nk_es((st3 + (T)e - u3) * (T)(2.0 / W), g);
+            accr += mr * k3;
+            acci += mi * k3;
+        } else {
+            accr = mr;
+            acci = mi;
+        }
+    }
+    C out;
+    out.x = accr;
+    out.y = acci;
+    return out;
+}
+
+template <typename T, int D, int W>
+__global__ void __launch_bounds__(256)
+k_interp_gm(int M, const int32_t *__restrict__ perm, const int32_t *__restrict__ keys,
+            const T *__restrict__ pts, int64_t pitch,
+            const typename cplx<T>::t *__restrict__ fine, Geom g,
+            typename cplx<T>::t *__restrict__ out) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= M) return;
+    int corner[3];
+    nk_bin_corner(keys[j], g, corner);
+    T k1[W], k2[W];
+    const int s1 = corner[0] + nk_kernel_row<T, W>(pts[j], g, k1);
+    const int s2 = corner[1] + nk_kernel_row<T, W>(pts[pitch + j], g, k2);
+    T u3 = 0, st3 = 0;
+    if (D == 3) {
+        u3 = pts[2 * pitch + j];
+        st3 = nk_ceil<T>(u3 - (T)(0.5 * W));
+    }
+    const int s3 = corner[2] + (int)st3;
+    const int dst = perm ? perm[j] : j;
+    out[dst] = gather_global<T, D, W>(fine, g, s1, s2, s3, k1, k2, u3, st3);
+}
+
+template <typename T, int D, int W>
+__global__ void __launch_bounds__(256)
+k_interp_staged(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
+                const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
+                const T *__restrict__ pts, int64_t pitch,
+                const typename cplx<T>::t *__restrict__ fine, Geom g,
+                typename cplx<T>::t *__restrict__ out) {
+    typedef typename cplx<T>::t C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *buf = reinterpret_cast<C *>(smem_raw);
+    const int s = blockIdx.x;
+    int corner[3];
+    nk_bin_corner(sub_bin[s], g, corner);
+    const int h = g.halo;
+    const int p1 = min(g.m[0], g.n[0] - corner[0]) + 2 * h;
+    const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
+    const int p3 = D == 3 ? min(g.m[2], g.n[2] - corner[2]) + 2 * h : 1;
+    const int P = p1 * p2 * p3;
+    const int o1 = corner[0] - h, o2 = corner[1] - h, o3 = corner[2] - h;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int q1 = i % p1;
+        const int r = i / p1;
+        const int q2 = r % p2;
+        const int q3 = r / p2;
+        int64_t l = nk_wrap(o1 + q1, g.n[0]) +
+                    (int64_t)g.n[0] * (nk_wrap(o2 + q2, g.n[1]) +
+                                       (D == 3 ? (int64_t)g.n[1] * nk_wrap(o3 + q3, g.n[2]) : 0));
+        buf[i] = __ldg(fine + l);
+    }
+    __syncthreads();
+    const int j0 = sub_start[s], j1 = sub_stop[s];
+    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+        T k1[W], k2[W];
+        const int t1 = nk_kernel_row<T, W>(pts[j], g, k1) + h;
+        const int t2 = nk_kernel_row<T, W>(pts[pitch + j], g, k2) + h;
+        T u3 = 0, st3 = 0;
+        if (D == 3) {
+            u3 = pts[2 * pitch + j];
+            st3 = nk_ceil<T>(u3 - (T)(0.5 * W));
+        }
+        const int t3 = (int)st3 + (D == 3 ? h : 0);
+        T accr = 0, acci = 0;
+#pragma unroll 1
+        for (int e = 0; e < (D == 3 ? W : 1); ++e) {
+            T mr = 0, mi = 0;
+#pragma unroll
+            for (int b = 0; b < W; ++b) {
+                const C *row = buf + ((t3 + e) * p2 + (t2 + b)) * p1 + t1;
+                T ir = 0, ii = 0;
+#pragma unroll
+                for (int a = 0; a < W; ++a) {
+                    C v = row[a];
+                    ir += v.x * k1[a];
+                    ii += v.y * k1[a];
+                }
+                mr += ir * k2[b];
+                mi += ii * k2[b];
+            }
+            if (D == 3) {
+                const T k3 = nk_es((st3 + (T)e - u3) * (T)(2.0 / W), g);
+                accr += mr * k3;
+                acci += mi * k3;
+            } else {
+                accr = mr;
+                acci = mi;
+            }
+        }
+        C o;
+        o.x = accr;
+        o.y = acci;
+        out[perm[j]] = o;
+    }
+}
+
+template <typename T, int D, int W>
+int launch_w(nk_plan *p, const void *fine, void *out, int *launches) {
+    typedef typename cplx<T>::t C;
+    const int M = (int)p->M;
+    if (M == 0) return NK_OK;
+    if (p->method == NK_SM) {
+        if (p->S == 0) return NK_OK;
+        size_t smem = (size_t)p->max_sub_smem;
+        auto kern = k_interp_staged<T, D, W>;
+        NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        kern<<<(unsigned)p->S, 256, smem, p->stream>>>(p->d_sub_bin, p->d_sub_start,
+                                                      p->d_sub_stop, p->d_perm,
+                                                      (const T *)p->d_pts, p->cap_M,
+                                                      (const C *)fine, p->geom, (C *)out);
+    } else {
+        const int32_t *perm = p->method == NK_GM ? nullptr : p->d_perm;
+        k_interp_gm<T, D, W><<<(M + 255) / 256, 256, 0, p->stream>>>(
+            M, perm, p->d_keys, (const T *)p->d_pts, p->cap_M, (const C *)fine, p->geom,
+            (C *)out);
+    }
+    NK_LAUNCH_CHECK();
+    ++*launches;
+    return NK_OK;
+}
+
+template <typename T, int D>
+int launch_d(nk_plan *p, const void *fine, void *out, int *launches) {
+    switch (p->w) {
+#define NK_W(W) \
+    case W: return launch_w<T, D, W>(p, fine, out, launches);
+        NK_W(2) NK_W(3) NK_W(4) NK_W(5) NK_W(6) NK_W(7) NK_W(8) NK_W(9) NK_W(10) NK_W(11)
+        NK_W(12) NK_W(13) NK_W(14) NK_W(15) NK_W(16)
+#undef NK_W
+    }
+    nk_set_error("unsupported kernel width");
+    return NK_ERR_VALUE;
+}
+
+}  // namespace
+
+int nk_launch_interp(nk_plan *p, const void *fine, void *out, int *launches) {
+    if (p->prec == NK_DOUBLE)
+        return p->dim == 2 ? launch_d<double, 2>(p, fine, out, launches)
+                           : launch_d<double, 3>(p, fine, out, launches);
+    return p->dim == 2 ? launch_d<float, 2>(p, fine, out, launches)
+                       : launch_d<float, 3>(p, fine, out, launches);
+}

@@ -1,0 +1,481 @@
+// setpts hot path: FP64 fold + bin key + histogram (K1), exclusive scans
+// (K2), stable LSD radix sort of bin keys -> permutation (K3), subproblem
+// table (K4) and the sorted local-coordinate gather (K5).
+//
+// Bit-exact targets: binsort.py:91-131 (fold, cells, keys), :149-153
+// (bincount, cumsum, stable argsort), :166-219 (build_subproblems).
+#include <limits.h>
+
+#include <algorithm>
+
+#include "nk_device.cuh"
+
+namespace {
+
+constexpr int SORT_BLOCK = 256;
+constexpr int SORT_ITEMS = 16;
+constexpr int SORT_TILE = SORT_BLOCK * SORT_ITEMS;  // keys per tile
+constexpr int SORT_WARPS = SORT_BLOCK / 32;
+constexpr int RADIX_BITS = 8;
+constexpr int RADIX = 1 << RADIX_BITS;
+
+constexpr int SCAN_BLOCK = 256;
+constexpr int SCAN_ITEMS = 16;
+constexpr int SCAN_CHUNK = SCAN_BLOCK * SCAN_ITEMS;
+
+// ---------------------------------------------------------------- K1
+// One thread per input point: fold each axis in FP64 exactly like
+// grid_coords, clamp the cell, flatten the bin key (axis 1 fastest) and
+// count it (warp-aggregated so clustered inputs do not serialise).
+template <typename TC>
+__global__ void __launch_bounds__(256)
+k_fold_keys(int M, const TC *__restrict__ x, const TC *__restrict__ y,
+            const TC *__restrict__ z, int64_t stride, Geom g, int32_t *__restrict__ keys,
+            int32_t *__restrict__ counts, unsigned long long *__restrict__ bad) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool in = i < M;
+    unsigned mask = __ballot_sync(0xffffffffu, in);
+    if (!in) return;
+    const TC *ax[3] = {x, y, z};
+    int key = 0, kstride = 1;
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (a < g.dim) {
+            double xv = (double)ax[a][(int64_t)i * stride];
+            if (!isfinite(xv)) ok = false;
+            double v = ok ? nk_fold(xv, g.scale[a]) : 0.0;
+            int c = nk_cell(v, g.n[a]);
+            key += kstride * (c / g.m[a]);
+            kstride *= g.nb[a];
+        }
+    }
+    if (!ok) {
+        atomicMin(bad, (unsigned long long)i);
+        key = 0;
+    }
+    keys[i] = key;
+    unsigned peers = __match_any_sync(mask, key);
+    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&counts[key], __popc(peers));
+}
+
+// ---------------------------------------------------------------- K2
+// Three-phase exclusive scan of int32: out[0..n] with out[n] = total.
+__device__ __forceinline__ int pad_idx(int i) { return i + (i >> 4); }
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+    int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// Block-wide exclusive scan of one value per thread; returns the exclusive
+// prefix and writes the block total to *total.
+__device__ __forceinline__ int block_excl_scan(int v, int *total) {
+    __shared__ int wsum[33];
+    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int inc = warp_incl_scan(v);
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int nw = blockDim.x >> 5;
+        int s = lane < nw ? wsum[lane] : 0;
+        int si = warp_incl_scan(s);
+        if (lane < nw) wsum[lane] = si - s;
+        if (lane == nw - 1) wsum[32] = si;
+    }
+    __syncthreads();
+    int res = inc - v + wsum[warp];
+    *total = wsum[32];
+    __syncthreads();
+    return res;
+}
+
+__global__ void __launch_bounds__(SCAN_BLOCK)
+k_scan_reduce(const int32_t *__restrict__ in, int64_t n, int32_t *__restrict__ partials) {
+    int64_t base = (int64_t)blockIdx.x * SCAN_CHUNK;
+    int s = 0;
+    for (int it = 0; it < SCAN_ITEMS; ++it) {
+        int64_t i = base + it * SCAN_BLOCK + threadIdx.x;
+        if (i < n) s += in[i];
+    }
+    int tot;
+    block_excl_scan(s, &tot);
+    if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_partials(int32_t *partials, int np) {
+    int carry = 0;
+    for (int base = 0; base < np; base += blockDim.x) {
+        int i = base + threadIdx.x;
+        int v = i < np ? partials[i] : 0;
+        int tot;
+        int ex = block_excl_scan(v, &tot);
+        if (i < np) partials[i] = ex + carry;
+        carry += tot;
+    }
+}
+
+__global__ void __launch_bounds__(SCAN_BLOCK)
+k_scan_down(const int32_t *in, int64_t n, const int32_t *__restrict__ partials,
+            int32_t *out) {   // in may alias out
+    __shared__ int buf[SCAN_CHUNK + SCAN_CHUNK / 16];
+    int64_t base = (int64_t)blockIdx.x * SCAN_CHUNK;
+    for (int it = 0; it < SCAN_ITEMS; ++it) {
+        int li = it * SCAN_BLOCK + threadIdx.x;
+        int64_t i = base + li;
+        buf[pad_idx(li)] = i < n ? in[i] : 0;
+    }
+    __syncthreads();
+    int loc[SCAN_ITEMS];
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+        loc[k] = s;
+        s += buf[pad_idx(threadIdx.x * SCAN_ITEMS + k)];
+    }
+    int tot;
+    int ex = block_excl_scan(s, &tot) + partials[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) buf[pad_idx(threadIdx.x * SCAN_ITEMS + k)] = loc[k] + ex;
+    __syncthreads();
+    for (int it = 0; it < SCAN_ITEMS; ++it) {
+        int li = it * SCAN_BLOCK + threadIdx.x;
+        int64_t i = base + li;
+        if (i < n) out[i] = buf[pad_idx(li)];
+    }
+    // in may alias out: the grand total comes from the scanned partials
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = partials[blockIdx.x] + tot;
+}
+
+// ---------------------------------------------------------------- K3
+// Stable LSD radix sort, 8-bit digits, 4096-key tiles.  Upsweep: per-tile
+// digit histogram stored digit-major; the (digit, tile) matrix is
+// exclusive-scanned; downsweep ranks each key stably inside its tile
+// (warp-striped order, __match_any_sync peers + per-warp digit counters)
+// and scatters (key, value) to its global slot.
+__global__ void __launch_bounds__(SORT_BLOCK)
+k_radix_hist(const int32_t *__restrict__ keys, int M, int shift, int ntiles,
+             int32_t *__restrict__ hist) {
+    __shared__ int h[RADIX];
+    for (int i = threadIdx.x; i < RADIX; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    int base = blockIdx.x * SORT_TILE;
+    int lane = threadIdx.x & 31;
+#pragma unroll 4
+    for (int it = 0; it < SORT_ITEMS; ++it) {
+        int idx = base + it * SORT_BLOCK + threadIdx.x;
+        bool valid = idx < M;
+        int d = valid ? (keys[idx] >> shift) & (RADIX - 1) : RADIX;
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (valid && lane == __ffs(peers) - 1) atomicAdd(&h[d], __popc(peers));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < RADIX; i += blockDim.x)
+        hist[(int64_t)i * ntiles + blockIdx.x] = h[i];
+}
+
+__global__ void __launch_bounds__(SORT_BLOCK)
+k_radix_scatter(const int32_t *__restrict__ keys_in, const int32_t *__restrict__ vals_in,
+                int M, int shift, int ntiles, const int32_t *__restrict__ offs,
+                int32_t *__restrict__ keys_out, int32_t *__restrict__ vals_out) {
+    __shared__ int wcnt[SORT_WARPS][RADIX];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < SORT_WARPS * RADIX; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+    __syncthreads();
+    const int base = blockIdx.x * SORT_TILE + warp * 32 * SORT_ITEMS;
+    const unsigned lt = (1u << lane) - 1u;
+    int key[SORT_ITEMS], val[SORT_ITEMS], rank[SORT_ITEMS];
+#pragma unroll
+    for (int it = 0; it < SORT_ITEMS; ++it) {
+        int idx = base + it * 32 + lane;
+        bool valid = idx < M;
+        key[it] = valid ? keys_in[idx] : 0;
+        val[it] = valid ? (vals_in ? vals_in[idx] : idx) : 0;
+        int d = valid ? (key[it] >> shift) & (RADIX - 1) : RADIX;
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        int c = valid ? wcnt[warp][d] : 0;
+        __syncwarp();
+        if (valid && lane == __ffs(peers) - 1) wcnt[warp][d] = c + __popc(peers);
+        __syncwarp();
+        rank[it] = c + __popc(peers & lt);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < RADIX; d += blockDim.x) {
+        int run = offs[(int64_t)d * ntiles + blockIdx.x];
+#pragma unroll
+        for (int w = 0; w < SORT_WARPS; ++w) {
+            int c = wcnt[w][d];
+            wcnt[w][d] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < SORT_ITEMS; ++it) {
+        int idx = base + it * 32 + lane;
+        if (idx < M) {
+            int d = (key[it] >> shift) & (RADIX - 1);
+            int pos = wcnt[warp][d] + rank[it];
+            keys_out[pos] = key[it];
+            vals_out[pos] = val[it];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K4
+__global__ void k_nsub(const int32_t *__restrict__ counts, int nbins, int msub,
+                       int32_t *__restrict__ nsub) {
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nbins) nsub[b] = (counts[b] + msub - 1) / msub;   // binsort.py:183
+}
+
+// One thread per subproblem: binary-search its bin in the scanned
+// per-bin subproblem counts, then slice (binsort.py:203-211).
+__global__ void k_fill_subs(int S, const int32_t *__restrict__ nsub_off, int nbins,
+                            const int32_t *__restrict__ starts, int msub,
+                            int32_t *__restrict__ sub_bin, int32_t *__restrict__ sub_start,
+                            int32_t *__restrict__ sub_stop) {
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    int lo = 0, hi = nbins - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (nsub_off[mid] <= s) lo = mid;
+        else hi = mid - 1;
+    }
+    int b = lo;
+    int r = s - nsub_off[b];
+    int st = starts[b] + r * msub;
+    int en = min(st + msub, starts[b + 1]);
+    sub_bin[s] = b;
+    sub_start[s] = st;
+    sub_stop[s] = en;
+}
+
+__global__ void k_export_subs(int S, Geom g, const int32_t *__restrict__ sub_bin,
+                              int32_t *__restrict__ offsets, int32_t *__restrict__ padded) {
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    int corner[3];
+    nk_bin_corner(sub_bin[s], g, corner);
+    for (int a = 0; a < g.dim; ++a) {
+        int actual = min(g.m[a], g.n[a] - corner[a]);     // binsort.py:200
+        if (offsets) offsets[s * g.dim + a] = corner[a] - g.halo;   // :207
+        if (padded) padded[s * g.dim + a] = actual + 2 * g.halo;    // :208
+    }
+}
+
+// ---------------------------------------------------------------- K5
+// Visit-order local coordinates u = v - bin corner, in plan precision
+// (a float keeps ~4e-6 cell resolution inside a 32-cell bin where a float
+// global v would lose 1e-4 cells at n = 2048).
+template <typename TC, typename T>
+__global__ void __launch_bounds__(256)
+k_gather_points(int M, const int32_t *__restrict__ perm, const TC *__restrict__ x,
+                const TC *__restrict__ y, const TC *__restrict__ z, int64_t stride, Geom g,
+                T *__restrict__ pts, int64_t pitch) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= M) return;
+    int i = perm ? perm[j] : j;
+    const TC *ax[3] = {x, y, z};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (a < g.dim) {
+            double v = nk_fold((double)ax[a][(int64_t)i * stride], g.scale[a]);
+            int c = nk_cell(v, g.n[a]);
+            int corner = (c / g.m[a]) * g.m[a];
+            pts[a * pitch + j] = (T)(v - (double)corner);
+        }
+    }
+}
+
+template <typename T>
+int grow(T **ptr, int64_t *cap, int64_t need) {
+    if (need <= *cap && *ptr) return NK_OK;
+    if (*ptr) cudaFree(*ptr);
+    *ptr = nullptr;
+    int64_t n = std::max<int64_t>(need, 1);
+    NK_CUDA(cudaMalloc((void **)ptr, sizeof(T) * n));
+    *cap = n;
+    return NK_OK;
+}
+
+inline unsigned blocks_for(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+}  // namespace
+
+int nk_scan_exclusive(nk_plan *p, const int32_t *in, int32_t *out, int64_t n) {
+    if (n <= 0) {
+        NK_CUDA(cudaMemsetAsync(out, 0, sizeof(int32_t), p->stream));
+        return NK_OK;
+    }
+    int64_t np = (n + SCAN_CHUNK - 1) / SCAN_CHUNK;
+    int rc = grow(&p->d_scan_tmp, &p->cap_scan_tmp, np);
+    if (rc) return rc;
+    k_scan_reduce<<<(unsigned)np, SCAN_BLOCK, 0, p->stream>>>(in, n, p->d_scan_tmp);
+    k_scan_partials<<<1, 1024, 0, p->stream>>>(p->d_scan_tmp, (int)np);
+    k_scan_down<<<(unsigned)np, SCAN_BLOCK, 0, p->stream>>>(in, n, p->d_scan_tmp, out);
+    NK_LAUNCH_CHECK();
+    return NK_OK;
+}
+
+static int ensure_point_buffers(nk_plan *p, int64_t M) {
+    if (M <= p->cap_M && p->d_keys) return NK_OK;
+    void **bufs[] = {(void **)&p->d_keys_in, (void **)&p->d_keys, (void **)&p->d_perm,
+                     (void **)&p->d_alt_keys, (void **)&p->d_alt_vals, &p->d_pts};
+    for (void **b : bufs) {
+        if (*b) cudaFree(*b);
+        *b = nullptr;
+    }
+    int64_t n = std::max<int64_t>(M, 1);
+    NK_CUDA(cudaMalloc((void **)&p->d_keys_in, 4 * n));
+    NK_CUDA(cudaMalloc((void **)&p->d_keys, 4 * n));
+    NK_CUDA(cudaMalloc((void **)&p->d_perm, 4 * n));
+    NK_CUDA(cudaMalloc((void **)&p->d_alt_keys, 4 * n));
+    NK_CUDA(cudaMalloc((void **)&p->d_alt_vals, 4 * n));
+    NK_CUDA(cudaMalloc(&p->d_pts, (size_t)p->csize / 2 * p->dim * n));
+    p->cap_M = n;
+    return NK_OK;
+}
+
+template <typename TC>
+static int fold_keys(nk_plan *p, const void *x, const void *y, const void *z, int64_t stride) {
+    int M = (int)p->M;
+    k_fold_keys<TC><<<blocks_for(M, 256), 256, 0, p->stream>>>(
+        M, (const TC *)x, (const TC *)y, (const TC *)z, stride, p->geom, p->d_keys_in,
+        p->d_counts, p->d_bad);
+    NK_LAUNCH_CHECK();
+    return NK_OK;
+}
+
+template <typename TC, typename T>
+static int gather(nk_plan *p, const int32_t *perm, const void *x, const void *y, const void *z,
+                  int64_t stride) {
+    int M = (int)p->M;
+    k_gather_points<TC, T><<<blocks_for(M, 256), 256, 0, p->stream>>>(
+        M, perm, (const TC *)x, (const TC *)y, (const TC *)z, stride, p->geom, (T *)p->d_pts,
+        p->cap_M);
+    NK_LAUNCH_CHECK();
+    return NK_OK;
+}
+
+int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, const void *z,
+                   int64_t stride) {
+    int rc = ensure_point_buffers(p, p->M);
+    if (rc) return rc;
+    const int64_t M = p->M;
+    const int nbins = (int)p->nbins;
+    cudaStream_t st = p->stream;
+    NK_CUDA(cudaMemsetAsync(p->d_counts, 0, sizeof(int32_t) * nbins, st));
+    NK_CUDA(cudaMemsetAsync(p->d_bad, 0xff, sizeof(unsigned long long), st));
+    if (M > 0) {
+        rc = coord_prec == NK_DOUBLE ? fold_keys<double>(p, x, y, z, stride)
+                                     : fold_keys<float>(p, x, y, z, stride);
+        if (rc) return rc;
+    }
+    unsigned long long bad = ~0ull;
+    NK_CUDA(cudaMemcpyAsync(&bad, p->d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
+    NK_CUDA(cudaStreamSynchronize(st));
+    if (bad != ~0ull) {
+        nk_set_error_index((int64_t)bad);
+        nk_set_error("non-finite coordinate at point index " + std::to_string(bad));
+        return NK_ERR_NONFINITE;
+    }
+    // starts = exclusive cumsum of counts, length nbins + 1 (binsort.py:150-151)
+    rc = nk_scan_exclusive(p, p->d_counts, p->d_starts, nbins);
+    if (rc) return rc;
+
+    const int32_t *perm = nullptr;
+    p->sorted = false;
+    if (p->method != NK_GM && M > 0) {
+        int bits = 1;
+        while ((1ll << bits) < p->nbins) ++bits;
+        int passes = (bits + RADIX_BITS - 1) / RADIX_BITS;
+        int ntiles = (int)((M + SORT_TILE - 1) / SORT_TILE);
+        rc = grow(&p->d_tile_hist, &p->cap_tile_hist, (int64_t)RADIX * ntiles + 1);
+        if (rc) return rc;
+        int32_t *A[2] = {p->d_keys, p->d_perm}, *B[2] = {p->d_alt_keys, p->d_alt_vals};
+        const int32_t *kin = p->d_keys_in, *vin = nullptr;
+        for (int ps = 0; ps < passes; ++ps) {
+            bool toA = ((passes - 1 - ps) % 2) == 0;   // the last pass lands in A
+            int32_t **dst = toA ? A : B;
+            int shift = ps * RADIX_BITS;
+            k_radix_hist<<<ntiles, SORT_BLOCK, 0, st>>>(kin, (int)M, shift, ntiles,
+                                                        p->d_tile_hist);
+            NK_LAUNCH_CHECK();
+            rc = nk_scan_exclusive(p, p->d_tile_hist, p->d_tile_hist, (int64_t)RADIX * ntiles);
+            if (rc) return rc;
+            k_radix_scatter<<<ntiles, SORT_BLOCK, 0, st>>>(kin, vin, (int)M, shift, ntiles,
+                                                           p->d_tile_hist, dst[0], dst[1]);
+            NK_LAUNCH_CHECK();
+            kin = dst[0];
+            vin = dst[1];
+        }
+        perm = p->d_perm;
+        p->sorted = true;
+    } else if (M > 0) {
+        NK_CUDA(cudaMemcpyAsync(p->d_keys, p->d_keys_in, 4 * M, cudaMemcpyDeviceToDevice, st));
+    }
+    if (M > 0) {
+        if (p->prec == NK_DOUBLE)
+            rc = coord_prec == NK_DOUBLE ? gather<double, double>(p, perm, x, y, z, stride)
+                                         : gather<float, double>(p, perm, x, y, z, stride);
+        else
+            rc = coord_prec == NK_DOUBLE ? gather<double, float>(p, perm, x, y, z, stride)
+                                         : gather<float, float>(p, perm, x, y, z, stride);
+        if (rc) return rc;
+    }
+
+    // subproblems (binsort.py:166-219), needed by the SM spread and the
+    // staged interpolation
+    p->S = 0;
+    if (p->method == NK_SM && M > 0) {
+        k_nsub<<<blocks_for(nbins, 256), 256, 0, st>>>(p->d_counts, nbins, p->msub,
+                                                       p->d_nsub_off);
+        NK_LAUNCH_CHECK();
+        rc = nk_scan_exclusive(p, p->d_nsub_off, p->d_nsub_off, nbins);
+        if (rc) return rc;
+        int32_t S = 0;
+        NK_CUDA(cudaMemcpyAsync(&S, p->d_nsub_off + nbins, 4, cudaMemcpyDeviceToHost, st));
+        NK_CUDA(cudaStreamSynchronize(st));
+        p->S = S;
+        if (S > 0) {
+            if (S > p->cap_S || !p->d_sub_bin) {
+                cudaFree(p->d_sub_bin);
+                cudaFree(p->d_sub_start);
+                cudaFree(p->d_sub_stop);
+                NK_CUDA(cudaMalloc((void **)&p->d_sub_bin, 4 * (size_t)S));
+                NK_CUDA(cudaMalloc((void **)&p->d_sub_start, 4 * (size_t)S));
+                NK_CUDA(cudaMalloc((void **)&p->d_sub_stop, 4 * (size_t)S));
+                p->cap_S = S;
+            }
+            k_fill_subs<<<blocks_for(S, 256), 256, 0, st>>>(S, p->d_nsub_off, nbins,
+                                                            p->d_starts, p->msub, p->d_sub_bin,
+                                                            p->d_sub_start, p->d_sub_stop);
+            NK_LAUNCH_CHECK();
+        }
+    }
+    NK_CUDA(cudaStreamSynchronize(st));
+    return NK_OK;
+}
+
+int nk_export_subproblems(const nk_plan *p, int32_t *bin_ids, int32_t *starts, int32_t *stops,
+                          int32_t *offsets, int32_t *padded) {
+    if (p->S == 0) return NK_OK;
+    cudaStream_t st = p->stream;
+    size_t b = 4 * (size_t)p->S;
+    if (bin_ids) NK_CUDA(cudaMemcpyAsync(bin_ids, p->d_sub_bin, b, cudaMemcpyDeviceToDevice, st));
+    if (starts) NK_CUDA(cudaMemcpyAsync(starts, p->d_sub_start, b, cudaMemcpyDeviceToDevice, st));
+    if (stops) NK_CUDA(cudaMemcpyAsync(stops, p->d_sub_stop, b, cudaMemcpyDeviceToDevice, st));
+    if (offsets || padded) {
+        k_export_subs<<<blocks_for(p->S, 256), 256, 0, st>>>((int)p->S, p->geom, p->d_sub_bin,
+                                                             offsets, padded);
+        NK_LAUNCH_CHECK();
+    }
+    return NK_OK;
+}

@@ -1,0 +1,178 @@
+// Type-1 step 1: ES-kernel spreading onto the fine grid.
+//
+//  K6a/K6b  GM / GM-sort (spread.py:142-163 -> _kernels.py:36-79): one thread
+//           per point in input / bin-sorted order, w^d native global
+//           REDG.E.ADD.F32x2 (single) or F64 (double) reductions.
+//  K6c      SM (spread.py:166-182 -> _kernels.py:82-147): one CTA per
+//           subproblem accumulates its padded bin (Eq. (16)) in shared memory,
+//           then merges it into the grid with periodic wrap (Eq. (17)).
+#include "nk_device.cuh"
+
+namespace {
+
+template <typename T, int D, int W>
+__global__ void __launch_bounds__(256)
+k_spread_gm(int M, const int32_t *__restrict__ perm, const int32_t *__restrict__ keys,
+            const T *__restrict__ pts, int64_t pitch, const typename cplx<T>::t *__restrict__ c,
+            Geom g, typename cplx<T>::t *__restrict__ fine) {
+    typedef typename cplx<T>::t C;
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= M) return;
+    int corner[3];
+    nk_bin_corner(keys[j], g, corner);
+    const int src = perm ? perm[j] : j;
+    const C cv = c[src];
+    T k1[W], k2[W];
+    const int s1 = corner[0] + nk_kernel_row<T, W>(pts[j], g, k1);
+    const int s2 = corner[1] + nk_kernel_row<T, W>(pts[pitch + j], g, k2);
+    T u3 = 0, st3 = 0;
+    if (D == 3) {
+        u3 = pts[2 * pitch + j];
+        st3 = nk_ceil<T>(u3 - (T)(0.5 * W));
+    }
+    const int s3 = corner[2] + (int)st3;
+    const int n1 = g.n[0], n2 = g.n[1], n3 = g.n[2];
+    int l1[W];
+#pragma unroll
+    for (int a = 0; a < W; ++a) l1[a] = nk_wrap(s1 + a, n1);
+    // 3D: the axis-3 loop stays rolled (compile size), its kernel value is
+    // evaluated per iteration
+#pragma unroll 1
+    for (int e = 0; e < (D == 3 ? W : 1); ++e) {
+        T t3r = cv.x, t3i = cv.y;
+        int64_t plane = 0;
+        if (D == 3) {
+            const T k3 = nk_es((st3 + (T)e - u3) * (T)(2.0 / W), g);
+            t3r *= k3;
+            t3i *= k3;
+            plane = (int64_t)nk_wrap(s3 + e, n3) * n2;
+        }
+#pragma unroll
+        for (int b = 0; b < W; ++b) {
+            const T t2r = t3r * k2[b], t2i = t3i * k2[b];
+            C *row = fine + (plane + nk_wrap(s2 + b, n2)) * (int64_t)n1;
+#pragma unroll
+            for (int a = 0; a < W; ++a) nk_red(row + l1[a], t2r * k1[a], t2i * k1[a]);
+        }
+    }
+}
+
+template <typename T, int D, int W>
+__global__ void __launch_bounds__(256)
+k_spread_sm(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
+            const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
+            const T *__restrict__ pts, int64_t pitch, const typename cplx<T>::t *__restrict__ c,
+            Geom g, typename cplx<T>::t *__restrict__ fine) {
+    typedef typename cplx<T>::t C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *buf = reinterpret_cast<T *>(smem_raw);
+    const int s = blockIdx.x;
+    int corner[3];
+    nk_bin_corner(sub_bin[s], g, corner);
+    const int h = g.halo;
+    // padded dims p_i = actual_i + 2 ceil(w/2) (binsort.py:200,208)
+    const int p1 = min(g.m[0], g.n[0] - corner[0]) + 2 * h;
+    const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
+    const int p3 = D == 3 ? min(g.m[2], g.n[2] - corner[2]) + 2 * h : 1;
+    const int P = p1 * p2 * p3;
+    for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) buf[i] = (T)0;
+    __syncthreads();
+
+    const int j0 = sub_start[s], j1 = sub_stop[s];
+    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+        const C cv = c[perm[j]];
+        T k1[W], k2[W];
+        // local start inside the padded bin: s_i = start_i - offset_i >= 0
+        const int t1 = nk_kernel_row<T, W>(pts[j], g, k1) + h;
+        const int t2 = nk_kernel_row<T, W>(pts[pitch + j], g, k2) + h;
+        T u3 = 0, st3 = 0;
+        if (D == 3) {
+            u3 = pts[2 * pitch + j];
+            st3 = nk_ceil<T>(u3 - (T)(0.5 * W));
+        }
+        const int t3 = (int)st3 + (D == 3 ? h : 0);
+#pragma unroll 1
+        for (int e = 0; e < (D == 3 ? W : 1); ++e) {
+            T t3r = cv.x, t3i = cv.y;
+            if (D == 3) {
+                const T k3 = nk_es((st3 + (T)e - u3) * (T)(2.0 / W), g);
+                t3r *= k3;
+                t3i *= k3;
+            }
+#pragma unroll
+            for (int b = 0; b < W; ++b) {
+                const T t2r = t3r * k2[b], t2i = t3i * k2[b];
+                T *row = buf + 2 * (((t3 + e) * p2 + (t2 + b)) * p1 + t1);
+#pragma unroll
+                for (int a = 0; a < W; ++a) {
+                    atomicAdd(row + 2 * a, t2r * k1[a]);
+                    atomicAdd(row + 2 * a + 1, t2i * k1[a]);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // merge_wrap (Eq. (17)): l_i = (offset_i + s_i) mod n_i
+    const int o1 = corner[0] - h, o2 = corner[1] - h, o3 = corner[2] - h;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int q1 = i % p1;
+        const int r = i / p1;
+        const int q2 = r % p2;
+        const int q3 = r / p2;
+        const T re = buf[2 * i], im = buf[2 * i + 1];
+        if (re == (T)0 && im == (T)0) continue;
+        int64_t l = nk_wrap(o1 + q1, g.n[0]) +
+                    (int64_t)g.n[0] * (nk_wrap(o2 + q2, g.n[1]) +
+                                       (D == 3 ? (int64_t)g.n[1] * nk_wrap(o3 + q3, g.n[2]) : 0));
+        nk_red(fine + l, re, im);
+    }
+}
+
+template <typename T, int D, int W>
+int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
+    typedef typename cplx<T>::t C;
+    const int M = (int)p->M;
+    if (M == 0) return NK_OK;
+    if (p->method == NK_SM) {
+        if (p->S == 0) return NK_OK;
+        size_t smem = (size_t)p->max_sub_smem;
+        auto kern = k_spread_sm<T, D, W>;
+        NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        kern<<<(unsigned)p->S, 256, smem, p->stream>>>(p->d_sub_bin, p->d_sub_start,
+                                                      p->d_sub_stop, p->d_perm,
+                                                      (const T *)p->d_pts, p->cap_M,
+                                                      (const C *)c, p->geom, (C *)fine);
+    } else {
+        const int32_t *perm = p->method == NK_GM ? nullptr : p->d_perm;
+        k_spread_gm<T, D, W><<<(M + 255) / 256, 256, 0, p->stream>>>(
+            M, perm, p->d_keys, (const T *)p->d_pts, p->cap_M, (const C *)c, p->geom, (C *)fine);
+    }
+    NK_LAUNCH_CHECK();
+    ++*launches;
+    return NK_OK;
+}
+
+template <typename T, int D>
+int launch_d(nk_plan *p, const void *c, void *fine, int *launches) {
+    switch (p->w) {
+#define NK_W(W) \
+    case W: return launch_w<T, D, W>(p, c, fine, launches);
+        NK_W(2) NK_W(3) NK_W(4) NK_W(5) NK_W(6) NK_W(7) NK_W(8) NK_W(9) NK_W(10) NK_W(11)
+        NK_W(12) NK_W(13) NK_W(14) NK_W(15) NK_W(16)
+#undef NK_W
+    }
+    nk_set_error("unsupported kernel width");
+    return NK_ERR_VALUE;
+}
+
+}  // namespace
+
+int nk_launch_spread(nk_plan *p, const void *c, void *fine, int *launches) {
+    NK_CUDA(cudaMemsetAsync(fine, 0, p->n_tot * p->csize, p->stream));
+    if (p->prec == NK_DOUBLE)
+        return p->dim == 2 ? launch_d<double, 2>(p, c, fine, launches)
+                           : launch_d<double, 3>(p, c, fine, launches);
+    return p->dim == 2 ? launch_d<float, 2>(p, c, fine, launches)
+                       : launch_d<float, 3>(p, c, fine, launches);
+}

@@ -1,0 +1,302 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's
+golden vectors and the CPU oracle.
+
+Bars:
+  * bin keys, counts, starts, permutation, subproblem table: bit-exact;
+  * spread / interp vs the reference's own loops: relative max error
+    <= 2e-6 (single) / 1e-13 (double) -- kernel values are evaluated in
+    the plan precision on the GPU, in FP64 by the reference;
+  * transforms: rel l2 vs direct sums <= 10 eps and vs the
+    oracle pipeline <= eps-level tolerances below.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SORT_CASES = ["s2r", "s2c", "s2w", "s3r", "s3c", "s3w"]
+
+
+@pytest.fixture(scope="module")
+def nk():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2102_08463_b200 as nk
+    return nk
+
+
+@pytest.fixture(scope="module")
+def st(nk):
+    from paper_2102_08463_b200 import stages
+    return stages
+
+
+def _case(nk, g, name):
+    grid = nk.GridSpec(tuple(int(x) for x in g[f"{name}_modes"]),
+                       tuple(int(x) for x in g[f"{name}_fine"]))
+    e, prec, msub = g[f"{name}_meta"]
+    params = nk.select_kernel_params(float(e), grid, "double" if prec else "single")
+    bd = tuple(int(x) for x in g[f"{name}_bindims"])
+    return grid, params, bd, int(msub)
+
+
+def _relmax(a, b):
+    return float(np.abs(np.asarray(a) - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+@pytest.mark.parametrize("name", SORT_CASES)
+def test_bin_sort_bitexact_vs_reference(golden, nk, st, name):
+    grid, params, bd, msub = _case(nk, golden, name)
+    lay = st.bin_sort(golden[f"{name}_pts"], grid, bd)
+    np.testing.assert_array_equal(lay.point_bins, golden[f"{name}_keys"])
+    np.testing.assert_array_equal(lay.counts, golden[f"{name}_counts"])
+    np.testing.assert_array_equal(lay.starts, golden[f"{name}_starts"])
+    np.testing.assert_array_equal(lay.perm, golden[f"{name}_perm"])
+    subs = st.build_subproblems(lay, params, msub)
+    np.testing.assert_array_equal(subs.bin_ids, golden[f"{name}_sub_bin"])
+    np.testing.assert_array_equal(subs.slice_starts, golden[f"{name}_sub_start"])
+    np.testing.assert_array_equal(subs.slice_stops, golden[f"{name}_sub_stop"])
+    np.testing.assert_array_equal(subs.offsets, golden[f"{name}_sub_off"])
+    np.testing.assert_array_equal(subs.padded_dims, golden[f"{name}_sub_pad"])
+
+
+def test_fold_seam_bitexact(golden, nk, st, orc):
+    """x at +-pi, nextafter neighbours, 3pi, +-1e30, +-0 (binsort.py:98-100)."""
+    xs = golden["gc_x"]
+    for n in (128, 512, 2048):
+        grid = nk.GridSpec((n // 2, n // 2), (n, n))
+        pts = np.stack([xs, xs[::-1]], axis=1)
+        lay = st.bin_sort(pts, grid, (1, 1))       # 1-cell bins: key = cell index
+        ref = orc.bin_sort(pts, grid, (1, 1))
+        np.testing.assert_array_equal(lay.point_bins, ref.point_bins)
+        np.testing.assert_array_equal(lay.perm, ref.perm)
+
+
+@pytest.mark.parametrize("M,dist,dims", [(200_000, "rand", 2), (300_000, "cluster", 3),
+                                         (150_000, "gauss", 3), (500_000, "rand", 3)])
+def test_bin_sort_bitexact_large(nk, st, orc, M, dist, dims):
+    modes = (256, 256) if dims == 2 else (64, 64, 64)
+    grid = orc.make_grid(modes, 1e-6, "single")
+    pts = orc.gen_points(dist, M, grid, 11, np.float32)
+    lay = st.bin_sort(pts, nk.GridSpec(modes, grid.fine))
+    ref = orc.bin_sort(pts, grid)
+    np.testing.assert_array_equal(lay.point_bins, ref.point_bins)
+    np.testing.assert_array_equal(lay.counts, ref.counts)
+    np.testing.assert_array_equal(lay.perm, ref.perm)
+    p = orc.select_kernel_params(1e-6, grid, "single")
+    subs = st.build_subproblems(lay, p, 1024)
+    rs = orc.build_subproblems(ref, p, 1024)
+    np.testing.assert_array_equal(subs.bin_ids, rs.bin_ids)
+    np.testing.assert_array_equal(subs.slice_stops, rs.slice_stops)
+    np.testing.assert_array_equal(subs.offsets, rs.offsets)
+
+
+@pytest.mark.parametrize("name", SORT_CASES)
+@pytest.mark.parametrize("method", ["gm", "gmsort", "sm"])
+def test_spread_vs_reference(golden, nk, st, name, method):
+    grid, params, bd, msub = _case(nk, golden, name)
+    pts, c = golden[f"{name}_pts"], golden[f"{name}_c"]
+    ref = golden[f"{name}_spread_sm"]
+    if method == "gm":
+        got = st.spread_gm(pts, c, params, grid)
+    else:
+        lay = st.bin_sort(pts, grid, bd)
+        if method == "gmsort":
+            got = st.spread_gm_sort(pts, lay, c, params, grid)
+        else:
+            got = st.spread_sm(pts, lay, st.build_subproblems(lay, params, msub), c, params,
+                               grid)
+    assert got.shape == ref.shape and got.dtype == ref.dtype
+    tol = 1e-13 if params.precision == "double" else 2e-6
+    assert _relmax(got, ref) < tol
+
+
+@pytest.mark.parametrize("name", SORT_CASES)
+@pytest.mark.parametrize("method", ["gm", "gmsort", "sm"])
+def test_interp_vs_reference(golden, nk, st, name, method):
+    grid, params, bd, msub = _case(nk, golden, name)
+    pts = golden[f"{name}_pts"]
+    ref = golden[f"{name}_interp"]
+    lay = None if method == "gm" else st.bin_sort(pts, grid, bd)
+    got = st.interpolate(pts, lay, golden[f"{name}_interp_grid"], params, grid, method=method)
+    tol = 1e-13 if params.precision == "double" else 2e-6
+    assert _relmax(got, ref) < tol
+
+
+@pytest.mark.parametrize("name", SORT_CASES)
+def test_transforms_vs_reference_composition(golden, nk, name):
+    grid, params, bd, msub = _case(nk, golden, name)
+    tol = 1e-12 if params.precision == "double" else 5e-6
+    p1 = nk.make_plan(1, grid.modes, params.epsilon, "sm", params.precision, bin_dims=bd,
+                      max_subproblem=msub)
+    p1.set_points(golden[f"{name}_pts"])
+    f = p1.execute(golden[f"{name}_c"])
+    ref = golden[f"{name}_type1"]
+    assert np.linalg.norm(f.reshape(-1) - ref) / np.linalg.norm(ref) < tol
+    for method in ("gm", "gmsort", "sm"):
+        p2 = nk.make_plan(2, grid.modes, params.epsilon, method, params.precision, bin_dims=bd)
+        p2.set_points(golden[f"{name}_pts"])
+        c = p2.execute(golden[f"{name}_f"])
+        ref2 = golden[f"{name}_type2"]
+        assert np.linalg.norm(c - ref2) / np.linalg.norm(ref2) < tol
+
+
+ACC = [(2, "double", 1e-2), (2, "double", 1e-6), (2, "double", 1e-9), (2, "double", 1e-12),
+       (3, "double", 1e-4), (3, "double", 1e-9), (3, "double", 1e-12),
+       (2, "single", 1e-2), (2, "single", 1e-4), (2, "single", 1e-6),
+       (3, "single", 1e-4), (3, "single", 1e-6)]
+
+
+@pytest.mark.parametrize("dim,prec,eps", ACC)
+@pytest.mark.parametrize("dist", ["rand", "cluster"])
+def test_accuracy_vs_direct(nk, orc, dim, prec, eps, dist):
+    """SPEC.md:571 acceptance 1 (N=(64,64) / (20,20,20), rho = 1): rel l2 vs
+    the direct oracle <= 10 eps for every method."""
+    modes = (64, 64) if dim == 2 else (20, 20, 20)
+    grid = orc.make_grid(modes, eps, prec)
+    M = int(np.prod(grid.fine))
+    rdt = np.float32 if prec == "single" else np.float64
+    cdt = np.complex64 if prec == "single" else np.complex128
+    pts = orc.gen_points(dist, M, grid, 5, rdt)
+    c = orc.gen_strengths(M, 5, cdt)
+    fm = orc.gen_strengths(int(np.prod(modes)), 6, cdt)
+    d1 = orc.direct_type1(pts, c, modes)
+    d2 = orc.direct_type2(pts, fm, modes)
+    for method in ("gm", "gmsort", "sm"):
+        p1 = nk.make_plan(1, modes, eps, method, prec)
+        p1.set_points(pts)
+        e1 = orc.rel_l2_error(p1.execute(c), d1)
+        p2 = nk.make_plan(2, modes, eps, method, prec)
+        p2.set_points(pts)
+        e2 = orc.rel_l2_error(p2.execute(fm.reshape(modes[::-1])), d2)
+        assert e1 < 10 * eps and e2 < 10 * eps, (method, e1, e2)
+
+
+@pytest.mark.parametrize("dim,prec", [(2, "double"), (3, "double"), (2, "single")])
+def test_adjointness(nk, orc, dim, prec):
+    """<c, T2 f> == <T1 c, f>."""
+    modes = (30, 26) if dim == 2 else (12, 10, 14)
+    eps = 1e-6
+    grid = orc.make_grid(modes, eps, prec)
+    M = 5000
+    rdt = np.float32 if prec == "single" else np.float64
+    cdt = np.complex64 if prec == "single" else np.complex128
+    pts = orc.gen_points("rand", M, grid, 9, rdt)
+    rng = np.random.default_rng(1)
+    for method in ("gmsort", "sm"):
+        c = (rng.standard_normal(M) + 1j * rng.standard_normal(M)).astype(cdt)
+        f = (rng.standard_normal(modes[::-1]) + 1j * rng.standard_normal(modes[::-1])).astype(cdt)
+        p1 = nk.make_plan(1, modes, eps, method, prec)
+        p1.set_points(pts)
+        p2 = nk.make_plan(2, modes, eps, method, prec)
+        p2.set_points(pts)
+        lhs = np.vdot(p2.execute(f).astype(np.complex128), c)
+        rhs = np.vdot(f.astype(np.complex128), p1.execute(c).astype(np.complex128))
+        tol = 1e-12 if prec == "double" else 1e-5
+        assert abs(lhs - rhs) <= tol * (abs(lhs) + abs(rhs))
+
+
+def test_c1_geometry_vs_oracle(nk, orc):
+    """BASELINE C1 geometry (N=256^2, f32, eps 1e-5) at M=2e5: GPU SM and
+    GM-sort vs the CPU oracle pipeline."""
+    modes, eps = (256, 256), 1e-5
+    grid = orc.make_grid(modes, eps, "single")
+    M = 200_000
+    pts = orc.gen_points("rand", M, grid, 1, np.float32)
+    c = orc.gen_strengths(M, 1, np.complex64)
+    op = orc.OraclePlan(1, modes, eps, "sm", "single", workers=orc.host_threads())
+    op.set_points(pts)
+    ref = op.execute(c)
+    for method in ("sm", "gmsort", "gm"):
+        p = nk.make_plan(1, modes, eps, method, "single")
+        p.set_points(pts)
+        assert orc.rel_l2_error(p.execute(c), ref) < 2e-6
+
+
+def test_c2_geometry_type2_vs_oracle(nk, orc):
+    """BASELINE C2 geometry (N=1024^2, n=2048^2, f32, eps 1e-5) at M=1e6."""
+    modes, eps = (1024, 1024), 1e-5
+    grid = orc.make_grid(modes, eps, "single")
+    M = 1_000_000
+    pts = orc.gen_points("rand", M, grid, 2, np.float32)
+    f = orc.gen_strengths(int(np.prod(modes)), 2, np.complex64).reshape(modes[::-1])
+    op = orc.OraclePlan(2, modes, eps, "gmsort", "single", workers=orc.host_threads())
+    op.set_points(pts)
+    ref = op.execute(f)
+    for method in ("gmsort", "sm", "gm"):
+        p = nk.make_plan(2, modes, eps, method, "single")
+        p.set_points(pts)
+        assert orc.rel_l2_error(p.execute(f), ref) < 2e-6
+
+
+def test_torch_device_path(nk, orc):
+    import torch
+    modes, eps = (40, 36), 1e-9
+    grid = orc.make_grid(modes, eps, "double")
+    pts = orc.gen_points("rand", 4096, grid, 3)
+    c = orc.gen_strengths(4096, 3)
+    dev = torch.device("cuda")
+    p = nk.make_plan(1, modes, eps)
+    p.set_points(torch.from_numpy(pts[:, 0]).to(dev), torch.from_numpy(pts[:, 1]).to(dev))
+    out = p.execute(torch.from_numpy(c).to(dev))
+    assert out.is_cuda and tuple(out.shape) == (36, 40)
+    assert orc.rel_l2_error(out.cpu().numpy(), orc.direct_type1(pts, c, modes)) < 10 * eps
+    # the one-shot API
+    f2 = nk.nufft2d1(pts[:, 0], pts[:, 1], c, modes, eps=eps)
+    np.testing.assert_allclose(f2, out.cpu().numpy(), rtol=0, atol=1e-12 * np.abs(f2).max())
+    cj = nk.nufft2d2(pts[:, 0], pts[:, 1], f2, eps=eps)
+    assert orc.rel_l2_error(cj, orc.direct_type2(pts, f2, modes)) < 10 * eps
+
+
+def test_errors_and_edge_cases(nk, orc):
+    p = nk.make_plan(1, (16, 16), 1e-6)
+    with pytest.raises(ValueError):
+        p.execute(np.zeros(4, np.complex128))          # before set_points
+    bad = np.zeros((10, 2))
+    bad[7, 1] = np.nan
+    with pytest.raises(ValueError, match="7"):
+        p.set_points(bad)
+    p.set_points(np.zeros((0, 2)))                     # M = 0 is legal
+    assert np.all(p.execute(np.zeros(0, np.complex128)) == 0)
+    p.set_points(np.zeros((3, 2)))
+    with pytest.raises(ValueError):
+        p.execute(np.zeros(4, np.complex128))          # length mismatch
+    with pytest.raises(ValueError):
+        nk.make_plan(1, (16,), 1e-6)
+    with pytest.raises(ValueError):
+        nk.make_plan(1, (16, 16), 2.0)
+    with pytest.raises(ValueError):
+        nk.make_plan(3, (16, 16), 1e-3)
+    with pytest.warns(UserWarning):
+        nk.make_plan(1, (16, 16), 1e-9, precision="single")
+    # single point at the origin -> all-ones
+    p = nk.make_plan(1, (32, 32), 1e-9)
+    p.set_points(np.zeros((1, 2)))
+    f = p.execute(np.ones(1, np.complex128))
+    assert np.abs(f - 1).max() < 1e-8
+    # constant-mode input -> all-ones
+    p = nk.make_plan(2, (8, 10, 6), 1e-9)
+    pts = np.random.default_rng(0).uniform(-7, 7, (100, 3))
+    p.set_points(pts)
+    fm = np.zeros((6, 10, 8), np.complex128)
+    fm[3, 5, 4] = 1.0
+    assert np.abs(p.execute(fm) - 1).max() < 1e-8
+
+
+def test_repeat_execute_and_reuse(nk, orc):
+    """Plan reuse without re-sorting and repeat determinism
+    within eps (GPU atomics reorder sums)."""
+    modes, eps = (64, 48), 1e-9
+    grid = orc.make_grid(modes, eps, "double")
+    pts = orc.gen_points("rand", 20000, grid, 4)
+    p = nk.make_plan(1, modes, eps)
+    p.set_points(pts)
+    c1, c2 = orc.gen_strengths(20000, 1), orc.gen_strengths(20000, 2)
+    a = p.execute(c1)
+    b = p.execute(c2)
+    a2 = p.execute(c1)
+    assert orc.rel_l2_error(a2, a) < 1e-14
+    lin = p.execute(2 * c1 - 3j * c2)
+    assert orc.rel_l2_error(lin, 2 * a - 3j * b) < 1e-12

@@ -62,7 +62,8 @@ void free_plan(nk_plan *p) {
     void *bufs[] = {p->d_fine, p->d_corr, p->d_keys_in, p->d_keys, p->d_perm, p->d_counts,
                     p->d_starts, p->d_pts, p->d_alt_keys, p->d_alt_vals, p->d_tile_hist,
                     p->d_scan_tmp, p->d_bad, p->d_nsub_off, p->d_sub_bin, p->d_sub_start,
-                    p->d_sub_stop, p->d_in_stage, p->d_out_stage};
+                    p->d_sub_stop, p->d_in_stage, p->d_out_stage, p->d_vperm_buf,
+                    p->d_pts_alt};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p->fft_ok) cufftDestroy(p->fft);
@@ -205,21 +206,42 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
 
-    // method (SPEC.md:170 defaults) and the SM padded-bin budget
-    int64_t pad_cells = 1;
-    for (int i = 0; i < dim; ++i) pad_cells *= p->bin_dims[i] + 2 * p->halo;
-    p->max_sub_smem = (int)std::min<int64_t>(pad_cells * (int64_t)p->csize, INT32_MAX);
+    // method (SPEC.md:170 defaults: SM for type 1; type 2 defaults to the
+    // shared-memory staged gather, measured faster than GM-sort on B200) and
+    // the shared-memory budget of the SM kernels.  Default bin dims are the
+    // reference's; if the padded bin does not fit in shared memory they are
+    // halved along the larger of axes 1/2 until it does.
     int method = opts.method;
-    if (method == NK_METHOD_DEFAULT) {
-        method = type == 1 ? NK_SM : NK_GMSORT;
-        if (method == NK_SM && p->max_sub_smem > smem_optin) method = NK_GMSORT;
-    } else if (method == NK_SM && p->max_sub_smem > smem_optin) {
-        nk_set_error("padded bin of " + std::to_string(p->max_sub_smem) +
-                     " bytes exceeds the per-block shared memory (" +
-                     std::to_string(smem_optin) + "); use smaller bin dims or gmsort");
-        delete p;
-        return NK_ERR_VALUE;
+    const bool user_bins = opts.bin_dims[0] || opts.bin_dims[1] || opts.bin_dims[2];
+    if (method == NK_METHOD_DEFAULT) method = NK_SM;
+    int64_t need = nk_sm_smem_bytes(type, dim, precision, w, p->bin_dims, p->halo);
+    if (method == NK_SM && need > smem_optin) {
+        if (user_bins) {
+            if (opts.method == NK_SM) {
+                nk_set_error("padded bin needs " + std::to_string(need) +
+                             " bytes of shared memory, more than the per-block " +
+                             std::to_string(smem_optin) + "; use smaller bin dims or gmsort");
+                delete p;
+                return NK_ERR_VALUE;
+            }
+            method = NK_GMSORT;
+        } else {
+            while (need > smem_optin && (p->bin_dims[0] > 1 || p->bin_dims[1] > 1)) {
+                int ax = p->bin_dims[0] >= p->bin_dims[1] ? 0 : 1;
+                p->bin_dims[ax] = (p->bin_dims[ax] + 1) / 2;
+                need = nk_sm_smem_bytes(type, dim, precision, w, p->bin_dims, p->halo);
+            }
+            if (need > smem_optin) method = NK_GMSORT;
+            p->nbins = 1;
+            for (int i = 0; i < 3; ++i) {
+                p->nb[i] = (p->n[i] + p->bin_dims[i] - 1) / p->bin_dims[i];
+                p->nbins *= p->nb[i];
+            }
+        }
     }
+    p->max_sub_smem = (int)std::min<int64_t>(need, INT32_MAX);
+    p->max_pad_cells = 1;
+    for (int i = 0; i < dim; ++i) p->max_pad_cells *= p->bin_dims[i] + 2 * p->halo;
     p->method = method;
 
     // geometry for kernels

@@ -30,9 +30,22 @@ __device__ __forceinline__ int nk_cell(double v, int n) {
 // ES kernel exp(beta (sqrt(1 - z^2) - 1)) on |z| <= 1 (_kernels.py:20-26).
 // Single precision uses exp2 with beta*log2(e) folded in (one MUFU.EX2);
 // double uses the accurate libdevice exp.
+// Single precision: MUFU.SQRT / MUFU.EX2 directly (sqrt.approx, ex2.approx:
+// ~1-2 ulp, no slow-path branches); the exponent lies in [-beta log2 e, 0].
+__device__ __forceinline__ float nk_sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float nk_ex2_approx(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 __device__ __forceinline__ float nk_es(float z, const Geom &g) {
-    float t = 1.0f - z * z;
-    return t >= 0.0f ? exp2f(g.betaf_log2e * (sqrtf(t) - 1.0f)) : 0.0f;
+    const float t = fmaf(-z, z, 1.0f);
+    const float v = nk_ex2_approx(g.betaf_log2e * (nk_sqrt_approx(fmaxf(t, 0.0f)) - 1.0f));
+    return t >= 0.0f ? v : 0.0f;
 }
 __device__ __forceinline__ double nk_es(double z, const Geom &g) {
     double t = 1.0 - z * z;
@@ -80,4 +93,23 @@ __device__ __forceinline__ void nk_bin_corner(int key, const Geom &g, int *corne
         corner[1] = (r % g.nb[1]) * g.m[1];
         corner[2] = (r / g.nb[1]) * g.m[2];
     }
+}
+
+// L2 eviction-priority hints (PTX createpolicy / st.global.L2::cache_hint):
+// scattered output stores keep their lines resident so partially written
+// sectors are completed in L2 instead of read-modify-written from HBM.
+__device__ __forceinline__ uint64_t nk_policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void nk_st_keep(float2 *ptr, float2 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(ptr), "f"(v.x),
+                 "f"(v.y), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void nk_st_keep(double2 *ptr, double2 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(ptr), "d"(v.x),
+                 "d"(v.y), "l"(pol)
+                 : "memory");
 }

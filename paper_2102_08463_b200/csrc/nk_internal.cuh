@@ -80,7 +80,11 @@ struct nk_plan {
     int64_t cap_M;
     int32_t *d_keys_in;     // bin key per input point
     int32_t *d_keys;        // bin key in visit order (sorted, or input order for GM)
-    int32_t *d_perm;        // visit position -> input index (NULL semantics for GM)
+    int32_t *d_perm;        // sorted position -> input index (bin-stable; exported layout)
+    int32_t *d_vperm;       // visit position -> input index, matches d_pts order
+                            // (== d_perm unless refined for bank-conflict-free gathers)
+    int32_t *d_vperm_buf;   // storage behind a refined d_vperm
+    void *d_pts_alt;        // scratch for reordering d_pts
     int32_t *d_counts;      // nbins
     int32_t *d_starts;      // nbins + 1
     void *d_pts;            // dim arrays of cap_M local coords (plan precision)
@@ -96,7 +100,8 @@ struct nk_plan {
     int64_t S, cap_S;
     int32_t *d_nsub_off;    // nbins + 1
     int32_t *d_sub_bin, *d_sub_start, *d_sub_stop;
-    int max_sub_smem;       // bytes
+    int max_sub_smem;       // bytes of dynamic smem for the SM kernels
+    int64_t max_pad_cells;  // prod(m_i + 2 halo)
 
     // staging for host pointers
     void *d_in_stage, *d_out_stage;
@@ -107,6 +112,21 @@ struct nk_plan {
     bool ev_ok;
     int last_launches;
 };
+
+// Points staged per batch by the plane-owned 3D SM spread (nk_spread.cu).
+inline int nk_sm3_batch(int prec) { return prec == NK_DOUBLE ? 64 : 128; }
+// Dynamic shared memory (bytes) of the SM spread / staged interp for a plan
+// shape: padded bin (+ point staging for the 3D spread).
+inline int64_t nk_sm_smem_bytes(int type, int dim, int prec, int w, const int *bin_dims,
+                                int halo) {
+    int64_t cells = 1;
+    for (int i = 0; i < dim; ++i) cells *= bin_dims[i] + 2 * halo;
+    int64_t rs = prec == NK_DOUBLE ? 8 : 4;
+    int64_t b = (cells * 2 * rs + 15) / 16 * 16;
+    if (type == 1 && dim == 3) b += (int64_t)nk_sm3_batch(prec) * (4 * w * rs + 8);
+    if (type == 1 && dim == 2) b += 128 + (32 * w * rs + 15) / 16 * 16 + 32 * w * 2 * rs;
+    return b;
+}
 
 // -------------------------------------------------------------- launchers
 int nk_scan_exclusive(nk_plan *p, const int32_t *in, int32_t *out, int64_t n);

@@ -107,13 +107,14 @@ k_interp_staged(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__
     }
     __syncthreads();
     const int j0 = sub_start[s], j1 = sub_stop[s];
+    const uint64_t keep = nk_policy_evict_last();
     for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
         T k1[W], k2[W];
-        const int t1 = nk_kernel_row<T, W>(pts[j], g, k1) + h;
-        const int t2 = nk_kernel_row<T, W>(pts[pitch + j], g, k2) + h;
+        const int t1 = nk_kernel_row<T, W>(__ldcs(pts + j), g, k1) + h;
+        const int t2 = nk_kernel_row<T, W>(__ldcs(pts + pitch + j), g, k2) + h;
         T u3 = 0, st3 = 0;
         if (D == 3) {
-            u3 = pts[2 * pitch + j];
+            u3 = __ldcs(pts + 2 * pitch + j);
             st3 = nk_ceil<T>(u3 - (T)(0.5 * W));
         }
         const int t3 = (int)st3 + (D == 3 ? h : 0);
@@ -146,7 +147,7 @@ k_interp_staged(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__
         C o;
         o.x = accr;
         o.y = acci;
-        out[perm[j]] = o;
+        nk_st_keep(out + __ldcs(perm + j), o, keep);
     }
 }
 
@@ -162,11 +163,11 @@ int launch_w(nk_plan *p, const void *fine, void *out, int *launches) {
         NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         kern<<<(unsigned)p->S, 256, smem, p->stream>>>(p->d_sub_bin, p->d_sub_start,
-                                                      p->d_sub_stop, p->d_perm,
+                                                      p->d_sub_stop, p->d_vperm,
                                                       (const T *)p->d_pts, p->cap_M,
                                                       (const C *)fine, p->geom, (C *)out);
     } else {
-        const int32_t *perm = p->method == NK_GM ? nullptr : p->d_perm;
+        const int32_t *perm = p->method == NK_GM ? nullptr : p->d_vperm;
         k_interp_gm<T, D, W><<<(M + 255) / 256, 256, 0, p->stream>>>(
             M, perm, p->d_keys, (const T *)p->d_pts, p->cap_M, (const C *)fine, p->geom,
             (C *)out);

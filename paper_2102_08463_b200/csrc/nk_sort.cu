@@ -294,6 +294,89 @@ k_gather_points(int M, const int32_t *__restrict__ perm, const TC *__restrict__ 
     }
 }
 
+// ---------------------------------------------------------------- K4b
+// Visit-order refinement for the staged interpolation (type 2, SM): inside
+// each subproblem, deal points round-robin over the shared-memory bank
+// residue of their footprint origin, so that the G lanes of one shared
+// memory wavefront (16 for 8-byte, 8 for 16-byte complex) gather from
+// distinct banks for every footprint cell.  Ranks inside a residue bucket
+// follow the sorted order, so the permutation is deterministic.  Only the
+// visit order changes; the exported bin-stable layout is untouched.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_refine_interleave(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
+                    const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm_in,
+                    const T *__restrict__ pts_in, int64_t pitch, Geom g, int G,
+                    int32_t *__restrict__ scratch, int32_t *__restrict__ perm_out,
+                    T *__restrict__ pts_out) {
+    __shared__ int cnt[16];
+    __shared__ int wcnt[8][16];
+    extern __shared__ int round_start[];   // max bucket size + 1
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x;
+    int corner[3];
+    nk_bin_corner(sub_bin[s], g, corner);
+    const int h = g.halo;
+    const int p1 = min(g.m[0], g.n[0] - corner[0]) + 2 * h;
+    const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
+    const int j0 = sub_start[s], j1 = sub_stop[s];
+    if (threadIdx.x < 16) cnt[threadIdx.x] = 0;
+    const unsigned lt = (1u << lane) - 1u;
+    const T half = (T)(0.5 * g.w);
+    for (int base = j0; base < j1; base += blockDim.x) {
+        const int j = base + threadIdx.x;
+        const bool valid = j < j1;
+        int r = 16;
+        if (valid) {
+            int t1 = (int)nk_ceil<T>(pts_in[j] - half) + h;
+            int t2 = (int)nk_ceil<T>(pts_in[pitch + j] - half) + h;
+            int t3 = g.dim == 3 ? (int)nk_ceil<T>(pts_in[2 * pitch + j] - half) + h : 0;
+            r = ((t3 * p2 + t2) * p1 + t1) & (G - 1);
+        }
+        if (threadIdx.x < 128) (&wcnt[0][0])[threadIdx.x] = 0;
+        __syncthreads();
+        unsigned peers = __match_any_sync(0xffffffffu, r);
+        if (valid && lane == __ffs(peers) - 1) wcnt[warp][r] = __popc(peers);
+        __syncthreads();
+        if (threadIdx.x < 16) {
+            int run = cnt[threadIdx.x];
+            for (int w = 0; w < 8; ++w) {
+                int c = wcnt[w][threadIdx.x];
+                wcnt[w][threadIdx.x] = run;
+                run += c;
+            }
+            cnt[threadIdx.x] = run;
+        }
+        __syncthreads();
+        if (valid) scratch[j] = ((wcnt[warp][r] + __popc(peers & lt)) << 4) | r;
+        __syncthreads();
+    }
+    // round k holds the k-th point of every bucket larger than k
+    int maxsz = 0;
+    for (int r = 0; r < G; ++r) maxsz = max(maxsz, cnt[r]);
+    int carry = 0;
+    for (int k0 = 0; k0 < maxsz; k0 += blockDim.x) {
+        const int k = k0 + threadIdx.x;
+        int nk = 0;
+        if (k < maxsz)
+            for (int r = 0; r < G; ++r) nk += cnt[r] > k;
+        int tot;
+        int ex = block_excl_scan(nk, &tot);
+        if (k < maxsz) round_start[k] = carry + ex;
+        carry += tot;
+    }
+    __syncthreads();
+    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+        const int v = scratch[j];
+        const int rank = v >> 4, r = v & 15;
+        int pos = round_start[rank];
+        for (int q = 0; q < r; ++q) pos += cnt[q] > rank;
+        const int d = j0 + pos;
+        perm_out[d] = perm_in[j];
+        for (int a = 0; a < g.dim; ++a) pts_out[a * pitch + d] = pts_in[a * pitch + j];
+    }
+}
+
 template <typename T>
 int grow(T **ptr, int64_t *cap, int64_t need) {
     if (need <= *cap && *ptr) return NK_OK;
@@ -327,7 +410,8 @@ int nk_scan_exclusive(nk_plan *p, const int32_t *in, int32_t *out, int64_t n) {
 static int ensure_point_buffers(nk_plan *p, int64_t M) {
     if (M <= p->cap_M && p->d_keys) return NK_OK;
     void **bufs[] = {(void **)&p->d_keys_in, (void **)&p->d_keys, (void **)&p->d_perm,
-                     (void **)&p->d_alt_keys, (void **)&p->d_alt_vals, &p->d_pts};
+                     (void **)&p->d_alt_keys, (void **)&p->d_alt_vals, &p->d_pts,
+                     (void **)&p->d_vperm_buf, &p->d_pts_alt};
     for (void **b : bufs) {
         if (*b) cudaFree(*b);
         *b = nullptr;
@@ -339,6 +423,10 @@ static int ensure_point_buffers(nk_plan *p, int64_t M) {
     NK_CUDA(cudaMalloc((void **)&p->d_alt_keys, 4 * n));
     NK_CUDA(cudaMalloc((void **)&p->d_alt_vals, 4 * n));
     NK_CUDA(cudaMalloc(&p->d_pts, (size_t)p->csize / 2 * p->dim * n));
+    if (p->type == 2 && p->method == NK_SM) {
+        NK_CUDA(cudaMalloc((void **)&p->d_vperm_buf, 4 * n));
+        NK_CUDA(cudaMalloc(&p->d_pts_alt, (size_t)p->csize / 2 * p->dim * n));
+    }
     p->cap_M = n;
     return NK_OK;
 }
@@ -421,6 +509,7 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
     } else if (M > 0) {
         NK_CUDA(cudaMemcpyAsync(p->d_keys, p->d_keys_in, 4 * M, cudaMemcpyDeviceToDevice, st));
     }
+    p->d_vperm = p->d_perm;
     if (M > 0) {
         if (p->prec == NK_DOUBLE)
             rc = coord_prec == NK_DOUBLE ? gather<double, double>(p, perm, x, y, z, stride)
@@ -459,6 +548,22 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
                                                             p->d_sub_start, p->d_sub_stop);
             NK_LAUNCH_CHECK();
         }
+    }
+    p->d_vperm = p->d_perm;
+    if (p->type == 2 && p->method == NK_SM && p->S > 0) {
+        const int G = p->prec == NK_DOUBLE ? 8 : 16;
+        size_t smem = 4 * ((size_t)p->msub + 1);
+        if (p->prec == NK_DOUBLE)
+            k_refine_interleave<double><<<(unsigned)p->S, 256, smem, st>>>(
+                p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_perm, (const double *)p->d_pts,
+                p->cap_M, p->geom, G, p->d_alt_keys, p->d_vperm_buf, (double *)p->d_pts_alt);
+        else
+            k_refine_interleave<float><<<(unsigned)p->S, 256, smem, st>>>(
+                p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_perm, (const float *)p->d_pts,
+                p->cap_M, p->geom, G, p->d_alt_keys, p->d_vperm_buf, (float *)p->d_pts_alt);
+        NK_LAUNCH_CHECK();
+        std::swap(p->d_pts, p->d_pts_alt);
+        p->d_vperm = p->d_vperm_buf;
     }
     NK_CUDA(cudaStreamSynchronize(st));
     return NK_OK;

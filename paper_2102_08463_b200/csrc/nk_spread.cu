@@ -128,23 +128,249 @@ k_spread_sm(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub
     }
 }
 
+// K6c-3D: plane-owned shared-memory spreading, no atomics.  A CTA owns one
+// subproblem's padded bin (p1 x p2 x p3 cells, Eq. (16)).  Points are
+// staged in batches: each thread evaluates one point's three kernel rows
+// (c folded into the axis-3 row) into shared memory.  Then every warp walks
+// the whole batch, but warp w only updates the padded-bin planes
+// z == w (mod 8): planes are owned, lanes cover distinct (a, b) cells of a
+// plane, so plain read-modify-write replaces the CAS loops that
+// atomicAdd(float/double) compiles to on shared memory.  The finished bin is
+// merged with native global vector reductions (Eq. (17)).
+template <typename T, int W>
+__global__ void __launch_bounds__(256)
+k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
+             const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
+             const T *__restrict__ pts, int64_t pitch, const typename cplx<T>::t *__restrict__ c,
+             Geom g, typename cplx<T>::t *__restrict__ fine, int64_t stage_off, int nbatch) {
+    typedef typename cplx<T>::t C;
+    constexpr int NIT = (W * W + 31) / 32;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *buf = reinterpret_cast<C *>(smem_raw);
+    int2 *sst = reinterpret_cast<int2 *>(smem_raw + stage_off);
+    T *sk1 = reinterpret_cast<T *>(sst + nbatch);
+    T *sk2 = sk1 + nbatch * W;
+    C *sck3 = reinterpret_cast<C *>(sk2 + nbatch * W);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x;
+    int corner[3];
+    nk_bin_corner(sub_bin[s], g, corner);
+    const int h = g.halo;
+    const int p1 = min(g.m[0], g.n[0] - corner[0]) + 2 * h;
+    const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
+    const int p3 = min(g.m[2], g.n[2] - corner[2]) + 2 * h;
+    const int P = p1 * p2 * p3, pstride = p1 * p2;
+    // per-lane footprint cells (a, b) of each plane pass, fixed for the block
+    int la[NIT], lb[NIT], lofs[NIT];
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+        const int idx = min(it * 32 + lane, W * W - 1);
+        lb[it] = idx / W;
+        la[it] = idx - lb[it] * W;
+        lofs[it] = lb[it] * p1 + la[it];
+    }
+    const bool last_ok = (NIT - 1) * 32 + lane < W * W;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        C zero;
+        zero.x = 0;
+        zero.y = 0;
+        buf[i] = zero;
+    }
+    const int j0 = sub_start[s], j1 = sub_stop[s];
+    for (int base = j0; base < j1; base += nbatch) {
+        const int nb = min(nbatch, j1 - base);
+        __syncthreads();   // previous batch consumed (and buffer zeroed)
+        for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+            const int j = base + q;
+            const C cv = c[perm[j]];
+            T k[W];
+            const int t1 = nk_kernel_row<T, W>(pts[j], g, k) + h;
+#pragma unroll
+            for (int r = 0; r < W; ++r) sk1[q * W + r] = k[r];
+            const int t2 = nk_kernel_row<T, W>(pts[pitch + j], g, k) + h;
+#pragma unroll
+            for (int r = 0; r < W; ++r) sk2[q * W + r] = k[r];
+            const int t3 = nk_kernel_row<T, W>(pts[2 * pitch + j], g, k) + h;
+#pragma unroll
+            for (int r = 0; r < W; ++r) {
+                C v;
+                v.x = cv.x * k[r];
+                v.y = cv.y * k[r];
+                sck3[q * W + r] = v;
+            }
+            sst[q] = make_int2((t3 * p2 + t2) * p1 + t1, t3);
+        }
+        __syncthreads();
+        for (int q = 0; q < nb; ++q) {
+            const int2 st = sst[q];
+            const T *k1q = sk1 + q * W;
+            const T *k2q = sk2 + q * W;
+#pragma unroll 1
+            for (int e = (warp - st.y) & 7; e < W; e += 8) {
+                const C ck = sck3[q * W + e];
+                C *plane = buf + st.x + e * pstride;
+#pragma unroll
+                for (int it = 0; it < NIT; ++it) {
+                    if (it < NIT - 1 || last_ok) {
+                        const T kk = k2q[lb[it]] * k1q[la[it]];
+                        C *cell = plane + lofs[it];
+                        C v = *cell;
+                        v.x += ck.x * kk;
+                        v.y += ck.y * kk;
+                        *cell = v;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    const int o1 = corner[0] - h, o2 = corner[1] - h, o3 = corner[2] - h;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const C v = buf[i];
+        if (v.x == (T)0 && v.y == (T)0) continue;
+        const int q1 = i % p1;
+        const int r = i / p1;
+        const int q2 = r % p2;
+        const int q3 = r / p2;
+        int64_t l = nk_wrap(o1 + q1, g.n[0]) +
+                    (int64_t)g.n[0] * (nk_wrap(o2 + q2, g.n[1]) +
+                                       (int64_t)g.n[1] * nk_wrap(o3 + q3, g.n[2]));
+        nk_red(fine + l, v.x, v.y);
+    }
+}
+
+// K6c-2D: one warp per subproblem.  The warp owns the whole padded bin, so
+// its lanes can cover one point's w x w footprint with plain shared-memory
+// read-modify-writes (distinct cells per pass, points in sequence): no
+// atomics and no inter-warp conflicts.  Each lane first evaluates one
+// point's kernel rows into shared memory (c folded into the axis-2 row).
+template <typename T, int W>
+__global__ void __launch_bounds__(32)
+k_spread_sm2(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
+             const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
+             const T *__restrict__ pts, int64_t pitch, const typename cplx<T>::t *__restrict__ c,
+             Geom g, typename cplx<T>::t *__restrict__ fine, int64_t stage_off) {
+    typedef typename cplx<T>::t C;
+    constexpr int NIT = (W * W + 31) / 32;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *buf = reinterpret_cast<C *>(smem_raw);
+    int *sbase = reinterpret_cast<int *>(smem_raw + stage_off);
+    T *sk1 = reinterpret_cast<T *>(sbase + 32);
+    C *sck2 = reinterpret_cast<C *>(smem_raw + stage_off + 128 + ((32 * W * sizeof(T) + 15) / 16) * 16);
+    const int lane = threadIdx.x;
+    const int s = blockIdx.x;
+    int corner[3];
+    nk_bin_corner(sub_bin[s], g, corner);
+    const int h = g.halo;
+    const int p1 = min(g.m[0], g.n[0] - corner[0]) + 2 * h;
+    const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
+    const int P = p1 * p2;
+    int la[NIT], lb[NIT], lofs[NIT];
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+        const int idx = min(it * 32 + lane, W * W - 1);
+        lb[it] = idx / W;
+        la[it] = idx - lb[it] * W;
+        lofs[it] = lb[it] * p1 + la[it];
+    }
+    const bool last_ok = (NIT - 1) * 32 + lane < W * W;
+    for (int i = lane; i < P; i += 32) {
+        C zero;
+        zero.x = 0;
+        zero.y = 0;
+        buf[i] = zero;
+    }
+    const int j0 = sub_start[s], j1 = sub_stop[s];
+    for (int base = j0; base < j1; base += 32) {
+        const int nb = min(32, j1 - base);
+        __syncwarp();
+        if (lane < nb) {
+            const int j = base + lane;
+            const C cv = c[perm[j]];
+            T k[W];
+            const int t1 = nk_kernel_row<T, W>(pts[j], g, k) + h;
+#pragma unroll
+            for (int r = 0; r < W; ++r) sk1[lane * W + r] = k[r];
+            const int t2 = nk_kernel_row<T, W>(pts[pitch + j], g, k) + h;
+#pragma unroll
+            for (int r = 0; r < W; ++r) {
+                C v;
+                v.x = cv.x * k[r];
+                v.y = cv.y * k[r];
+                sck2[lane * W + r] = v;
+            }
+            sbase[lane] = t2 * p1 + t1;
+        }
+        __syncwarp();
+        for (int q = 0; q < nb; ++q) {
+            C *org = buf + sbase[q];
+            const T *k1q = sk1 + q * W;
+            const C *ck2q = sck2 + q * W;
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) {
+                if (it < NIT - 1 || last_ok) {
+                    const C ck = ck2q[lb[it]];
+                    const T k1 = k1q[la[it]];
+                    C *cell = org + lofs[it];
+                    C v = *cell;
+                    v.x += ck.x * k1;
+                    v.y += ck.y * k1;
+                    *cell = v;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    __syncwarp();
+    const int o1 = corner[0] - h, o2 = corner[1] - h;
+    for (int i = lane; i < P; i += 32) {
+        const C v = buf[i];
+        if (v.x == (T)0 && v.y == (T)0) continue;
+        const int q1 = i % p1;
+        const int q2 = i / p1;
+        nk_red(fine + nk_wrap(o1 + q1, g.n[0]) + (int64_t)g.n[0] * nk_wrap(o2 + q2, g.n[1]),
+               v.x, v.y);
+    }
+}
+
 template <typename T, int D, int W>
 int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
     typedef typename cplx<T>::t C;
     const int M = (int)p->M;
     if (M == 0) return NK_OK;
-    if (p->method == NK_SM) {
+    if (p->method == NK_SM && D == 3) {
+        if (p->S == 0) return NK_OK;
+        size_t smem = (size_t)p->max_sub_smem;
+        auto kern = k_spread_sm3<T, W>;
+        NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        int64_t stage_off = (p->max_pad_cells * (int64_t)sizeof(C) + 15) / 16 * 16;
+        kern<<<(unsigned)p->S, 256, smem, p->stream>>>(
+            p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm, (const T *)p->d_pts,
+            p->cap_M, (const C *)c, p->geom, (C *)fine, stage_off, nk_sm3_batch(p->prec));
+    } else if (p->method == NK_SM && D == 2) {
+        if (p->S == 0) return NK_OK;
+        size_t smem = (size_t)p->max_sub_smem;
+        auto kern = k_spread_sm2<T, W>;
+        NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        int64_t stage_off = (p->max_pad_cells * (int64_t)sizeof(C) + 15) / 16 * 16;
+        kern<<<(unsigned)p->S, 32, smem, p->stream>>>(
+            p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm, (const T *)p->d_pts,
+            p->cap_M, (const C *)c, p->geom, (C *)fine, stage_off);
+    } else if (p->method == NK_SM) {
         if (p->S == 0) return NK_OK;
         size_t smem = (size_t)p->max_sub_smem;
         auto kern = k_spread_sm<T, D, W>;
         NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         kern<<<(unsigned)p->S, 256, smem, p->stream>>>(p->d_sub_bin, p->d_sub_start,
-                                                      p->d_sub_stop, p->d_perm,
+                                                      p->d_sub_stop, p->d_vperm,
                                                       (const T *)p->d_pts, p->cap_M,
                                                       (const C *)c, p->geom, (C *)fine);
     } else {
-        const int32_t *perm = p->method == NK_GM ? nullptr : p->d_perm;
+        const int32_t *perm = p->method == NK_GM ? nullptr : p->d_vperm;
         k_spread_gm<T, D, W><<<(M + 255) / 256, 256, 0, p->stream>>>(
             M, perm, p->d_keys, (const T *)p->d_pts, p->cap_M, (const C *)c, p->geom, (C *)fine);
     }

@@ -280,11 +280,16 @@ def test_errors_and_edge_cases(nk, orc):
         nk.make_plan(3, (16, 16), 1e-3)
     with pytest.warns(UserWarning):
         nk.make_plan(1, (16, 16), 1e-9, precision="single")
-    # single point at the origin -> all-ones
+    # single point at the origin -> all-ones.  The reference's
+    # own max deviation here is 1.458e-8 (> 10 eps); the bar is parity with it.
     p = nk.make_plan(1, (32, 32), 1e-9)
     p.set_points(np.zeros((1, 2)))
     f = p.execute(np.ones(1, np.complex128))
-    assert np.abs(f - 1).max() < 1e-8
+    op = orc.OraclePlan(1, (32, 32), 1e-9, "sm", "double")
+    op.set_points(np.zeros((1, 2)))
+    ref = op.execute(np.ones(1, np.complex128))
+    assert np.abs(f - 1).max() <= max(1e-8, 1.01 * np.abs(ref - 1).max())
+    assert np.abs(f.reshape(-1) - ref).max() < 1e-13
     # constant-mode input -> all-ones
     p = nk.make_plan(2, (8, 10, 6), 1e-9)
     pts = np.random.default_rng(0).uniform(-7, 7, (100, 3))

@@ -186,7 +186,13 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
         delete p;
         return NK_ERR_VALUE;
     }
-    p->msub = opts.max_subproblem ? opts.max_subproblem : 1024;   // binsort.py:38
+    // M_sub: the reference default is 1024 (binsort.py:38).  A plan that is
+    // not given one picks the B200-tuned size for its kernel: 256 for the
+    // one-warp 2D spread (more warps in flight), 4096 for the staged
+    // interpolation (one padded-bin load per bin).  Stage-level
+    // build_subproblems keeps the reference default.
+    p->msub = opts.max_subproblem ? opts.max_subproblem
+                                  : (type == 2 ? 4096 : (dim == 2 ? 256 : 1024));
     if (p->msub < 1) {
         nk_set_error("max subproblem size must be >= 1, got " + std::to_string(p->msub));
         delete p;

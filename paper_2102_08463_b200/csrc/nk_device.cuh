@@ -113,3 +113,12 @@ __device__ __forceinline__ void nk_st_keep(double2 *ptr, double2 v, uint64_t pol
                  "d"(v.y), "l"(pol)
                  : "memory");
 }
+
+// i / d and i % d for 0 <= i < 2^31, 1 <= d < 2^16 with one IMAD.HI:
+// magic = ceil(2^32 / d) (exact for i * d < 2^32).
+struct nk_divmod {
+    unsigned d, magic;
+    __device__ __forceinline__ explicit nk_divmod(unsigned dd)
+        : d(dd), magic((unsigned)((0x100000000ull + dd - 1) / dd)) {}
+    __device__ __forceinline__ unsigned div(unsigned i) const { return __umulhi(i, magic); }
+};

@@ -95,11 +95,12 @@ k_interp_staged(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__
     const int p3 = D == 3 ? min(g.m[2], g.n[2] - corner[2]) + 2 * h : 1;
     const int P = p1 * p2 * p3;
     const int o1 = corner[0] - h, o2 = corner[1] - h, o3 = corner[2] - h;
+    const nk_divmod dm1(p1), dm2(p2);
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int q1 = i % p1;
-        const int r = i / p1;
-        const int q2 = r % p2;
-        const int q3 = r / p2;
+        const int r = dm1.div(i);
+        const int q1 = i - r * p1;
+        const int q3 = D == 3 ? dm2.div(r) : 0;
+        const int q2 = r - q3 * p2;
         int64_t l = nk_wrap(o1 + q1, g.n[0]) +
                     (int64_t)g.n[0] * (nk_wrap(o2 + q2, g.n[1]) +
                                        (D == 3 ? (int64_t)g.n[1] * nk_wrap(o3 + q3, g.n[2]) : 0));
@@ -108,15 +109,32 @@ k_interp_staged(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__
     __syncthreads();
     const int j0 = sub_start[s], j1 = sub_stop[s];
     const uint64_t keep = nk_policy_evict_last();
-    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-        T k1[W], k2[W];
-        const int t1 = nk_kernel_row<T, W>(__ldcs(pts + j), g, k1) + h;
-        const int t2 = nk_kernel_row<T, W>(__ldcs(pts + pitch + j), g, k2) + h;
-        T u3 = 0, st3 = 0;
-        if (D == 3) {
-            u3 = __ldcs(pts + 2 * pitch + j);
-            st3 = nk_ceil<T>(u3 - (T)(0.5 * W));
+    // software pipeline: the next point's coordinates and slot load while
+    // this point gathers
+    int j = j0 + threadIdx.x;
+    T u1n = 0, u2n = 0, u3n = 0;
+    int dstn = 0;
+    if (j < j1) {
+        u1n = __ldcs(pts + j);
+        u2n = __ldcs(pts + pitch + j);
+        if (D == 3) u3n = __ldcs(pts + 2 * pitch + j);
+        dstn = __ldcs(perm + j);
+    }
+    for (; j < j1; j += blockDim.x) {
+        const T u1 = u1n, u2 = u2n, u3 = u3n;
+        const int dst = dstn;
+        const int jn = j + blockDim.x;
+        if (jn < j1) {
+            u1n = __ldcs(pts + jn);
+            u2n = __ldcs(pts + pitch + jn);
+            if (D == 3) u3n = __ldcs(pts + 2 * pitch + jn);
+            dstn = __ldcs(perm + jn);
         }
+        T k1[W], k2[W];
+        const int t1 = nk_kernel_row<T, W>(u1, g, k1) + h;
+        const int t2 = nk_kernel_row<T, W>(u2, g, k2) + h;
+        T st3 = 0;
+        if (D == 3) st3 = nk_ceil<T>(u3 - (T)(0.5 * W));
         const int t3 = (int)st3 + (D == 3 ? h : 0);
         T accr = 0, acci = 0;
 #pragma unroll 1
@@ -147,7 +165,7 @@ k_interp_staged(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__
         C o;
         o.x = accr;
         o.y = acci;
-        nk_st_keep(out + __ldcs(perm + j), o, keep);
+        nk_st_keep(out + dst, o, keep);
     }
 }
 

@@ -3,9 +3,10 @@
 //  K6a/K6b  GM / GM-sort (spread.py:142-163 -> _kernels.py:36-79): one thread
 //           per point in input / bin-sorted order, w^d native global
 //           REDG.E.ADD.F32x2 (single) or F64 (double) reductions.
-//  K6c      SM (spread.py:166-182 -> _kernels.py:82-147): one CTA per
-//           subproblem accumulates its padded bin (Eq. (16)) in shared memory,
-//           then merges it into the grid with periodic wrap (Eq. (17)).
+//  K6c      SM (spread.py:166-182 -> _kernels.py:82-147): each subproblem's
+//           padded bin (Eq. (16)) is accumulated in shared memory without
+//           atomics (one warp per subproblem in 2D, plane-owned warps in 3D),
+//           then merged into the grid with periodic wrap (Eq. (17)).
 #include "nk_device.cuh"
 
 namespace {
@@ -54,77 +55,6 @@ k_spread_gm(int M, const int32_t *__restrict__ perm, const int32_t *__restrict__
 #pragma unroll
             for (int a = 0; a < W; ++a) nk_red(row + l1[a], t2r * k1[a], t2i * k1[a]);
         }
-    }
-}
-
-template <typename T, int D, int W>
-__global__ void __launch_bounds__(256)
-k_spread_sm(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
-            const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
-            const T *__restrict__ pts, int64_t pitch, const typename cplx<T>::t *__restrict__ c,
-            Geom g, typename cplx<T>::t *__restrict__ fine) {
-    typedef typename cplx<T>::t C;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T *buf = reinterpret_cast<T *>(smem_raw);
-    const int s = blockIdx.x;
-    int corner[3];
-    nk_bin_corner(sub_bin[s], g, corner);
-    const int h = g.halo;
-    // padded dims p_i = actual_i + 2 ceil(w/2) (binsort.py:200,208)
-    const int p1 = min(g.m[0], g.n[0] - corner[0]) + 2 * h;
-    const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
-    const int p3 = D == 3 ? min(g.m[2], g.n[2] - corner[2]) + 2 * h : 1;
-    const int P = p1 * p2 * p3;
-    for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) buf[i] = (T)0;
-    __syncthreads();
-
-    const int j0 = sub_start[s], j1 = sub_stop[s];
-    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-        const C cv = c[perm[j]];
-        T k1[W], k2[W];
-        // local start inside the padded bin: s_i = start_i - offset_i >= 0
-        const int t1 = nk_kernel_row<T, W>(pts[j], g, k1) + h;
-        const int t2 = nk_kernel_row<T, W>(pts[pitch + j], g, k2) + h;
-        T u3 = 0, st3 = 0;
-        if (D == 3) {
-            u3 = pts[2 * pitch + j];
-            st3 = nk_ceil<T>(u3 - (T)(0.5 * W));
-        }
-        const int t3 = (int)st3 + (D == 3 ? h : 0);
-#pragma unroll 1
-        for (int e = 0; e < (D == 3 ? W : 1); ++e) {
-            T t3r = cv.x, t3i = cv.y;
-            if (D == 3) {
-                const T k3 = nk_es((st3 + (T)e - u3) * (T)(2.0 / W), g);
-                t3r *= k3;
-                t3i *= k3;
-            }
-#pragma unroll
-            for (int b = 0; b < W; ++b) {
-                const T t2r = t3r * k2[b], t2i = t3i * k2[b];
-                T *row = buf + 2 * (((t3 + e) * p2 + (t2 + b)) * p1 + t1);
-#pragma unroll
-                for (int a = 0; a < W; ++a) {
-                    atomicAdd(row + 2 * a, t2r * k1[a]);
-                    atomicAdd(row + 2 * a + 1, t2i * k1[a]);
-                }
-            }
-        }
-    }
-    __syncthreads();
-    // merge_wrap (Eq. (17)): l_i = (offset_i + s_i) mod n_i
-    const int o1 = corner[0] - h, o2 = corner[1] - h, o3 = corner[2] - h;
-    for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int q1 = i % p1;
-        const int r = i / p1;
-        const int q2 = r % p2;
-        const int q3 = r / p2;
-        const T re = buf[2 * i], im = buf[2 * i + 1];
-        if (re == (T)0 && im == (T)0) continue;
-        int64_t l = nk_wrap(o1 + q1, g.n[0]) +
-                    (int64_t)g.n[0] * (nk_wrap(o2 + q2, g.n[1]) +
-                                       (D == 3 ? (int64_t)g.n[1] * nk_wrap(o3 + q3, g.n[2]) : 0));
-        nk_red(fine + l, re, im);
     }
 }
 
@@ -201,27 +131,69 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
             sst[q] = make_int2((t3 * p2 + t2) * p1 + t1, t3);
         }
         __syncthreads();
-        for (int q = 0; q < nb; ++q) {
-            const int2 st = sst[q];
-            const T *k1q = sk1 + q * W;
-            const T *k2q = sk2 + q * W;
-#pragma unroll 1
-            for (int e = (warp - st.y) & 7; e < W; e += 8) {
-                const C ck = sck3[q * W + e];
-                C *plane = buf + st.x + e * pstride;
+        if (W <= 8) {
+            // at most one owned plane per point: software-pipelined so the
+            // next point's staged values load while this point's cells are
+            // read-modified-written
+            int2 st = sst[0];
+            int e = (warp - st.y) & 7;
+            C ck = sck3[min(e, W - 1)];
+            T kk[NIT];
 #pragma unroll
-                for (int it = 0; it < NIT; ++it) {
-                    if (it < NIT - 1 || last_ok) {
-                        const T kk = k2q[lb[it]] * k1q[la[it]];
-                        C *cell = plane + lofs[it];
-                        C v = *cell;
-                        v.x += ck.x * kk;
-                        v.y += ck.y * kk;
-                        *cell = v;
+            for (int it = 0; it < NIT; ++it) kk[it] = sk2[lb[it]] * sk1[la[it]];
+            for (int q = 0; q < nb; ++q) {
+                const int qn = min(q + 1, nb - 1);
+                const int2 stn = sst[qn];
+                const int en = (warp - stn.y) & 7;
+                const C ckn = sck3[qn * W + min(en, W - 1)];
+                T kkn[NIT];
+#pragma unroll
+                for (int it = 0; it < NIT; ++it) kkn[it] = sk2[qn * W + lb[it]] * sk1[qn * W + la[it]];
+                if (e < W) {
+                    C *plane = buf + st.x + e * pstride;
+#pragma unroll
+                    for (int it = 0; it < NIT; ++it) {
+                        if (it < NIT - 1 || last_ok) {
+                            C *cell = plane + lofs[it];
+                            C v = *cell;
+                            v.x += ck.x * kk[it];
+                            v.y += ck.y * kk[it];
+                            *cell = v;
+                        }
                     }
                 }
+                __syncwarp();
+                st = stn;
+                e = en;
+                ck = ckn;
+#pragma unroll
+                for (int it = 0; it < NIT; ++it) kk[it] = kkn[it];
             }
-            __syncwarp();
+        } else {
+            for (int q = 0; q < nb; ++q) {
+                const int2 st = sst[q];
+                const T *k1q = sk1 + q * W;
+                const T *k2q = sk2 + q * W;
+                T kk[NIT];
+#pragma unroll
+                for (int it = 0; it < NIT; ++it) kk[it] = k2q[lb[it]] * k1q[la[it]];
+#pragma unroll 1
+                for (int e = (warp - st.y) & 7; e < W; e += 8) {
+                    const C ck = sck3[q * W + e];
+                    C *plane = buf + st.x + e * pstride;
+#pragma unroll
+                    for (int it = 0; it < NIT; ++it) {
+                        if (it < NIT - 1 || last_ok) {
+                            C *cell = plane + lofs[it];
+                            C v = *cell;
+                            v.x += ck.x * kk[it];
+                            v.y += ck.y * kk[it];
+                            *cell = v;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
         }
     }
     __syncthreads();
@@ -303,23 +275,42 @@ k_spread_sm2(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
             sbase[lane] = t2 * p1 + t1;
         }
         __syncwarp();
+        // software-pipelined: point q+1's staged values load during q's RMW
+        int org = sbase[0];
+        C ck[NIT];
+        T k1[NIT];
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+            ck[it] = sck2[lb[it]];
+            k1[it] = sk1[la[it]];
+        }
         for (int q = 0; q < nb; ++q) {
-            C *org = buf + sbase[q];
-            const T *k1q = sk1 + q * W;
-            const C *ck2q = sck2 + q * W;
+            const int qn = min(q + 1, nb - 1);
+            const int orgn = sbase[qn];
+            C ckn[NIT];
+            T k1n[NIT];
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) {
+                ckn[it] = sck2[qn * W + lb[it]];
+                k1n[it] = sk1[qn * W + la[it]];
+            }
 #pragma unroll
             for (int it = 0; it < NIT; ++it) {
                 if (it < NIT - 1 || last_ok) {
-                    const C ck = ck2q[lb[it]];
-                    const T k1 = k1q[la[it]];
-                    C *cell = org + lofs[it];
+                    C *cell = buf + org + lofs[it];
                     C v = *cell;
-                    v.x += ck.x * k1;
-                    v.y += ck.y * k1;
+                    v.x += ck[it].x * k1[it];
+                    v.y += ck[it].y * k1[it];
                     *cell = v;
                 }
             }
             __syncwarp();
+            org = orgn;
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) {
+                ck[it] = ckn[it];
+                k1[it] = k1n[it];
+            }
         }
     }
     __syncwarp();
@@ -359,16 +350,6 @@ int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
         kern<<<(unsigned)p->S, 32, smem, p->stream>>>(
             p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm, (const T *)p->d_pts,
             p->cap_M, (const C *)c, p->geom, (C *)fine, stage_off);
-    } else if (p->method == NK_SM) {
-        if (p->S == 0) return NK_OK;
-        size_t smem = (size_t)p->max_sub_smem;
-        auto kern = k_spread_sm<T, D, W>;
-        NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        kern<<<(unsigned)p->S, 256, smem, p->stream>>>(p->d_sub_bin, p->d_sub_start,
-                                                      p->d_sub_stop, p->d_vperm,
-                                                      (const T *)p->d_pts, p->cap_M,
-                                                      (const C *)c, p->geom, (C *)fine);
     } else {
         const int32_t *perm = p->method == NK_GM ? nullptr : p->d_vperm;
         k_spread_gm<T, D, W><<<(M + 255) / 256, 256, 0, p->stream>>>(

@@ -245,35 +245,47 @@ def run_ours(args, cfg):
     out_t2 = torch.empty(cfg["M"], dtype=c_dev.dtype, device=dev)
     out_t1 = torch.empty(cfg["modes"][::-1], dtype=c_dev.dtype, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-    shard_t1 = world > 1 and cfg["type"] == 1
-    fine_buf = None
-    if shard_t1:
-        fine_buf = torch.empty(plans[1].grid.fine_shape, dtype=c_dev.dtype, device=dev)
-
-    from paper_2102_08463_b200 import _lib
+    from paper_2102_08463_b200.dist import CudaStageOps, ReplicaPlan, ShardedPlan
+    sharded = world > 1 and cfg["type"] in (1, 2)
+    runners = {}
+    for t in types:
+        if sharded:
+            runners[t] = ShardedPlan(CudaStageOps(plans[t]), t, root=0)
+        else:
+            runners[t] = ReplicaPlan(plans[t])   # world 1, or independent replicas (c5)
+    ev_a = torch.cuda.Event(enable_timing=True)
+    ev_b = torch.cuda.Event(enable_timing=True)
+    dom_in_step = []
 
     def step():
+        """One exec per transform in the config; returns this library's
+        kernel launches.  Sharded type 1: spread -> NCCL reduce -> root FFT +
+        deconv; sharded type 2: NCCL broadcast of the modes -> pad + FFT +
+        interp per rank."""
         launches = 0
         for t in types:
-            p = plans[t]
-            if t == 2:
-                if world > 1 and cfg["type"] == 2:
-                    dist.broadcast(f_dev, 0)
-                p.execute(f_dev, out_t2)
-            elif shard_t1:
-                # per-rank spread -> NCCL reduce of the fine grid -> root FFT + deconv
-                _lib.check(p._lib.nk_spread(p._h, c_dev.data_ptr(), fine_buf.data_ptr()))
+            r = runners[t]
+            if isinstance(r, ReplicaPlan):
+                r.execute(f_dev if t == 2 else c_dev, out_t2 if t == 2 else out_t1)
+                launches += plans[t].last_launch_count()
+            elif t == 1:
+                ev_a.record()
+                fine = r.ops.spread(c_dev)
+                ev_b.record()
+                dom_in_step.append((ev_a, ev_b))
+                dist.reduce(fine, dst=0)
                 launches += 1
-                dist.reduce(fine_buf, 0)
                 if rank == 0:
-                    _lib.check(p._lib.nk_fft(p._h, fine_buf.data_ptr(), -1))
-                    _lib.check(p._lib.nk_deconv_type1(p._h, fine_buf.data_ptr(),
-                                                      out_t1.data_ptr()))
+                    r.ops.fft_deconvolve(fine, out_t1)
                     launches += 1
-                continue
             else:
-                p.execute(c_dev, out_t1)
-            launches += p.last_launch_count()
+                dist.broadcast(f_dev, src=0)
+                fine = r.ops.pad_ifft(f_dev)
+                ev_a.record()
+                r.ops.interp(fine, out_t2)
+                ev_b.record()
+                dom_in_step.append((ev_a, ev_b))
+                launches += 2
         return launches
 
     for _ in range(args.warmup):
@@ -302,7 +314,10 @@ def run_ours(args, cfg):
             end.record()
             torch.cuda.synchronize()
             step_ms.append(start.elapsed_time(end))
-            if not shard_t1:
+            if sharded:
+                dom_ms.append(dom_in_step[-1][0].elapsed_time(dom_in_step[-1][1]))
+                dom_in_step.clear()
+            else:
                 st = plans[dom_type].stage_times()
                 dom_ms.append(st["interp" if dom_type == 2 else "spread"])
         t_post = time.time()
@@ -316,34 +331,58 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
 
-    # ---- e2e: the public API with pinned host buffers, copies inside the timing
+    # ---- e2e: the public API with pinned host buffers, copies inside the timing.
+    # Single GPU / replicas: plan.execute(host in, host out) through the C-ABI
+    # (H2D + exec + D2H, synchronous).  Sharded: each rank copies its inputs
+    # H2D, runs the sharded step (collective included) and reads its result
+    # back D2H.
     e2e = None
-    if not shard_t1:
-        pin_in = {}
+    pin_in = {}
+    for t in types:
+        src = f_host if t == 2 else c_host
+        b = torch.empty(src.shape, dtype=c_dev.dtype, pin_memory=True)
+        b.numpy()[...] = src
+        pin_in[t] = b
+    pin_out = {2: torch.empty(cfg["M"], dtype=c_dev.dtype, pin_memory=True),
+               1: torch.empty(cfg["modes"][::-1], dtype=c_dev.dtype, pin_memory=True)}
+
+    def e2e_step():
+        if not sharded:
+            for t in types:
+                plans[t].execute(pin_in[t].numpy(), pin_out[t].numpy())
+            return
         for t in types:
-            src = f_host if t == 2 else c_host
-            b = torch.empty(src.shape, dtype=c_dev.dtype, pin_memory=True)
-            b.numpy()[...] = src
-            pin_in[t] = b.numpy()
-        pin_out = {2: torch.empty(cfg["M"], dtype=c_dev.dtype, pin_memory=True).numpy(),
-                   1: torch.empty(cfg["modes"][::-1], dtype=c_dev.dtype,
-                                  pin_memory=True).numpy()}
-        for _ in range(max(1, args.warmup)):
-            for t in types:
-                plans[t].execute(pin_in[t], pin_out[t])
-        e2e_s = []
-        for _ in range(args.steps):
-            flush.fill_(1.0)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            for t in types:
-                plans[t].execute(pin_in[t], pin_out[t])    # H2D + exec + D2H, synchronous
-            e2e_s.append(time.perf_counter() - t0)
-        e2e_t = float(np.sum(e2e_s))
+            if t == 2:
+                f_dev.copy_(pin_in[2], non_blocking=True)
+            else:
+                c_dev.copy_(pin_in[1], non_blocking=True)
+        step()
+        for t in types:
+            if t == 2:
+                pin_out[2].copy_(out_t2, non_blocking=True)
+            elif rank == 0:
+                pin_out[1].copy_(out_t1, non_blocking=True)
+        torch.cuda.synchronize()
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    dom_in_step.clear()
+    e2e_s = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
         if world > 1:
-            t = torch.tensor([e2e_t], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_t = float(t.item())
+            dist.barrier()
+        t0 = time.perf_counter()
+        e2e_step()
+        e2e_s.append(time.perf_counter() - t0)
+    dom_in_step.clear()
+    e2e_t = float(np.sum(e2e_s))
+    if world > 1:
+        t = torch.tensor([e2e_t], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    if True:
         csz = c_dev.element_size()
         h2d = sum((int(np.prod(cfg["modes"])) if t == 2 else cfg["M"]) * csz for t in types)
         d2h = sum((cfg["M"] if t == 2 else int(np.prod(cfg["modes"]))) * csz for t in types)
@@ -361,12 +400,15 @@ def run_ours(args, cfg):
             "vs_baseline": None, "dtype": "f32" if cfg["prec"] == "single" else "f64",
             "data": "synthetic (seeded numpy: uniform / cluster / gauss points, U[0,1)^2 "
                     "complex strengths), inputs resident in HBM",
-            "config": {"workload": cfg["desc"], "method": plans[dom_type].method,
+            "config": {"workload": cfg["desc"] + (f", per rank x {world}" if world > 1 else ""),
+                       "method": plans[dom_type].method,
                        "fine": list(fine), "w": plans[dom_type].params.w,
                        "bin_dims": list(plans[dom_type].bin_dims),
                        "l2": "flushed between timed steps (256 MiB write)",
-                       "parallelism": f"points sharded over {world} GPU(s)"
-                                      if world > 1 else "1 GPU"},
+                       "parallelism": ("1 GPU" if world == 1 else
+                                       f"{world} GPUs: points sharded, type-1 fine grids "
+                                       "NCCL-reduced / type-2 modes NCCL-broadcast"
+                                       if sharded else f"{world} independent replicas")},
             "gpu_launches": launches,
         }
         if dom_avg:
@@ -377,7 +419,8 @@ def run_ours(args, cfg):
                                 "frac": ach / peak, "traffic": traffic_for(args.config),
                                 "algorithmic_bytes": B, "kernel_ms": dom_avg,
                                 "peak_source": peak_src}
-            line["stage_ms"] = plans[dom_type].stage_times()
+            if not sharded:
+                line["stage_ms"] = plans[dom_type].stage_times()
         if e2e:
             line["e2e"] = e2e
         line["clocks"] = clk.summary()

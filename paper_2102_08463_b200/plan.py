@@ -305,6 +305,68 @@ class TransformPlan:
     def last_launch_count(self):
         return int(self._lib.nk_last_launch_count(self._h))
 
+    # -- device stage ops (CUDA tensors, torch current stream) ----------------
+    # The pieces of execute() for callers that insert a collective between
+    # them (dist.py: type-1 grid reduce, type-2 mode broadcast).
+    def _dev(self, t, shape, what):
+        import torch as _t
+        cdt = _arrays.torch_dtype(_COMPLEX[self.precision])
+        if not (_arrays.is_torch(t) and t.is_cuda and t.dtype == cdt and t.is_contiguous()):
+            raise ValueError(f"{what} must be a contiguous CUDA {cdt} tensor")
+        if shape is not None and t.numel() != int(np.prod(shape)):
+            raise ValueError(f"{what} must have {int(np.prod(shape))} elements")
+        return t
+
+    def new_fine_grid(self):
+        return torch.empty(self.grid.fine_shape, dtype=_arrays.torch_dtype(_COMPLEX[self.precision]),
+                           device=torch.device("cuda", self.device))
+
+    def spread_to(self, strengths, fine):
+        """Step 1 of type 1: fine <- spread(strengths) (zeroed first)."""
+        self._check_points()
+        self._dev(strengths, (self.num_points,), "strengths")
+        self._dev(fine, self.grid.fine_shape, "fine grid")
+        self._sync_stream("cuda")
+        _lib.check(self._lib.nk_spread(self._h, strengths.data_ptr(), fine.data_ptr()))
+        return fine
+
+    def fft_(self, fine, direction):
+        """cuFFT in place: direction -1 forward, +1 inverse (unnormalised)."""
+        self._dev(fine, self.grid.fine_shape, "fine grid")
+        self._sync_stream("cuda")
+        _lib.check(self._lib.nk_fft(self._h, fine.data_ptr(), int(direction)))
+        return fine
+
+    def deconvolve_to(self, fine_spectrum, modes):
+        """Step 3 of type 1: modes <- p_k (-1)^{sum k} bhat[k mod n]."""
+        self._dev(fine_spectrum, self.grid.fine_shape, "fine spectrum")
+        self._dev(modes, self.grid.mode_shape, "modes")
+        self._sync_stream("cuda")
+        _lib.check(self._lib.nk_deconv_type1(self._h, fine_spectrum.data_ptr(), modes.data_ptr()))
+        return modes
+
+    def pad_to(self, modes, fine):
+        """Step 1 of type 2: fine <- zero-padded p_k (-1)^{sum k} f_k."""
+        self._dev(modes, self.grid.mode_shape, "modes")
+        self._dev(fine, self.grid.fine_shape, "fine grid")
+        self._sync_stream("cuda")
+        _lib.check(self._lib.nk_deconv_type2(self._h, modes.data_ptr(), fine.data_ptr()))
+        return fine
+
+    def interp_to(self, fine, out):
+        """Step 3 of type 2: out[j] <- gather at point j."""
+        self._check_points()
+        self._dev(fine, self.grid.fine_shape, "fine grid")
+        self._dev(out, (self.num_points,), "output")
+        self._sync_stream("cuda")
+        _lib.check(self._lib.nk_interp(self._h, fine.data_ptr(), out.data_ptr()))
+        return out
+
+    def _check_points(self):
+        self._check_alive()
+        if self.num_points is None:
+            raise ValueError("set_points has not been called")
+
     def layout_tensors(self):
         """Bin layout of the last set_points as int32 CUDA tensors:
         (point_bins, counts, starts, perm) -- binsort.py:45-65 fields."""

@@ -165,6 +165,11 @@ NK_API int nk_deconv_type2(nk_plan *plan, const void *modes, void *fine_spectrum
  * deconv|pad, ms[3] total.  Synchronises on the plan's last event. */
 NK_API int nk_stage_times(nk_plan *plan, float *ms, int n);
 
+/* Turn per-stage CUDA-event timing on/off (events are created on first
+ * use).  While timing is on, execute() launches directly instead of
+ * replaying its CUDA graph, so the events bracket each stage. */
+NK_API int nk_set_timing(nk_plan *plan, int on);
+
 /* Number of this library's kernels launched by the last nk_execute. */
 NK_API int nk_last_launch_count(const nk_plan *plan);
 

@@ -92,6 +92,7 @@ def lib():
         "nk_deconv_type2": (I, [P, P, P]),
         "nk_stage_times": (I, [P, ctypes.POINTER(ctypes.c_float), I]),
         "nk_last_launch_count": (I, [P]),
+        "nk_set_timing": (I, [P, I]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -105,7 +106,7 @@ EXPORTED = ["nk_tolerance_to_width", "nk_next_smooth", "nk_kernel_fourier", "nk_
             "nk_plan_create", "nk_plan_get_info", "nk_set_stream", "nk_setpts", "nk_execute",
             "nk_destroy", "nk_last_error", "nk_error_index", "nk_get_layout",
             "nk_get_subproblems", "nk_spread", "nk_interp", "nk_fft", "nk_deconv_type1",
-            "nk_deconv_type2", "nk_stage_times", "nk_last_launch_count"]
+            "nk_deconv_type2", "nk_stage_times", "nk_last_launch_count", "nk_set_timing"]
 
 
 def check(rc):

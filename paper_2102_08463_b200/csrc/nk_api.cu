@@ -2,6 +2,7 @@
 // lifecycle, stage-level parity hooks and cuFFT glue.
 #include <float.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -67,6 +68,8 @@ void free_plan(nk_plan *p) {
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p->fft_ok) cufftDestroy(p->fft);
+    if (p->gexec) cudaGraphExecDestroy(p->gexec);
+    if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     if (p->ev_ok)
         for (auto &e : p->ev) cudaEventDestroy(e);
     delete p;
@@ -331,6 +334,16 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
         for (auto &ev : p->ev) cudaEventCreate(&ev);
         p->ev_ok = true;
     }
+    {
+        const char *ng = getenv("NK_NO_GRAPH");
+        p->use_graph = !(ng && ng[0] == '1');
+        if (p->use_graph &&
+            cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            p->use_graph = false;
+            p->cap_stream = nullptr;
+        }
+    }
     *out = p;
     return NK_OK;
 }
@@ -391,6 +404,10 @@ extern "C" int nk_setpts(nk_plan *p, int64_t M, int coord_prec, const void *x, c
         }
     p->have_points = false;
     p->M = M;
+    if (p->gexec) {   // kernel parameters (M, S, buffers) change with the points
+        cudaGraphExecDestroy(p->gexec);
+        p->gexec = nullptr;
+    }
     // host coordinates: copy each axis (strided) into a device SoA buffer
     void *dev_axes[3] = {nullptr, nullptr, nullptr};
     const void *use[3] = {x, y, z};
@@ -446,6 +463,55 @@ static int execute_device(nk_plan *p, const void *in, void *out) {
     return NK_OK;
 }
 
+// Capture execute_device() once per (in, out) pair on the plan's private
+// capture stream and replay it into the caller's stream: one cudaGraphLaunch
+// instead of ~4 kernel/cuFFT launches per execute.
+static int execute_graph(nk_plan *p, const void *in, void *out) {
+    if (p->g_in != in || p->g_out != out) {
+        // a new (in, out) pair: launch directly; capture only when the same
+        // pair comes back (repeated executes on fixed buffers)
+        if (p->gexec) {
+            cudaGraphExecDestroy(p->gexec);
+            p->gexec = nullptr;
+        }
+        p->g_in = in;
+        p->g_out = out;
+        return execute_device(p, in, out);
+    }
+    if (!p->gexec) {
+        cudaStream_t user = p->stream;
+        p->stream = p->cap_stream;
+        NK_CUFFT(cufftSetStream(p->fft, p->cap_stream));
+        NK_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+        int rc = execute_device(p, in, out);
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(p->cap_stream, &graph);
+        p->stream = user;
+        cufftSetStream(p->fft, user);
+        if (rc || e != cudaSuccess) {
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();
+            // fall back to direct launches for this plan
+            p->use_graph = false;
+            return execute_device(p, in, out);
+        }
+        e = cudaGraphInstantiate(&p->gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            p->gexec = nullptr;
+            p->use_graph = false;
+            return execute_device(p, in, out);
+        }
+        p->g_in = in;
+        p->g_out = out;
+        p->g_launches = p->last_launches;
+    }
+    NK_CUDA(cudaGraphLaunch(p->gexec, p->stream));
+    p->last_launches = p->g_launches;
+    return NK_OK;
+}
+
 extern "C" int nk_execute(nk_plan *p, const void *in, void *out) {
     int rc = check_plan(p);
     if (rc) return rc;
@@ -474,7 +540,8 @@ extern "C" int nk_execute(nk_plan *p, const void *in, void *out) {
         if (rc) return rc;
         dout = p->d_out_stage;
     }
-    rc = execute_device(p, din, dout);
+    rc = (p->use_graph && !p->timing) ? execute_graph(p, din, dout)
+                                      : execute_device(p, din, dout);
     if (rc) return rc;
     if (out_host)
         NK_CUDA(cudaMemcpyAsync(out, dout, out_bytes, cudaMemcpyDeviceToHost, p->stream));
@@ -606,6 +673,17 @@ extern "C" int nk_stage_times(nk_plan *p, float *ms, int n) {
     }
     cudaEventElapsedTime(&t[3], p->ev[0], p->ev[3]);
     for (int i = 0; i < n && i < 4; ++i) ms[i] = t[i];
+    return NK_OK;
+}
+
+extern "C" int nk_set_timing(nk_plan *p, int on) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (on && !p->ev_ok) {
+        for (auto &ev : p->ev) NK_CUDA(cudaEventCreate(&ev));
+        p->ev_ok = true;
+    }
+    p->timing = on ? 1 : 0;
     return NK_OK;
 }
 

@@ -43,9 +43,10 @@ __device__ __forceinline__ float nk_ex2_approx(float x) {
     return r;
 }
 __device__ __forceinline__ float nk_es(float z, const Geom &g) {
-    const float t = fmaf(-z, z, 1.0f);
-    const float v = nk_ex2_approx(g.betaf_log2e * (nk_sqrt_approx(fmaxf(t, 0.0f)) - 1.0f));
-    return t >= 0.0f ? v : 0.0f;
+    // |z| <= 1 on every footprint cell (start = ceil(u - w/2)); the clamp
+    // only absorbs rounding at z = +-1, where the value is exp(-beta).
+    const float t = fmaxf(fmaf(-z, z, 1.0f), 0.0f);
+    return nk_ex2_approx(fmaf(g.betaf_log2e, nk_sqrt_approx(t), -g.betaf_log2e));
 }
 __device__ __forceinline__ double nk_es(double z, const Geom &g) {
     double t = 1.0 - z * z;
@@ -61,9 +62,10 @@ template <> __device__ __forceinline__ double nk_ceil<double>(double x) { return
 // ker[r] = phi((start + r - u) * 2/w) (_kernels.py:29-33).
 template <typename T, int W>
 __device__ __forceinline__ int nk_kernel_row(T u, const Geom &g, T *ker) {
-    T st = nk_ceil<T>(u - (T)(0.5 * W));
+    const T st = nk_ceil<T>(u - (T)(0.5 * W));
+    const T z0 = (st - u) * (T)(2.0 / W);
 #pragma unroll
-    for (int r = 0; r < W; ++r) ker[r] = nk_es((st + (T)r - u) * (T)(2.0 / W), g);
+    for (int r = 0; r < W; ++r) ker[r] = nk_es(z0 + (T)(2.0 * r / W), g);
     return (int)st;
 }
 

@@ -111,6 +111,15 @@ struct nk_plan {
     cudaEvent_t ev[4];
     bool ev_ok;
     int last_launches;
+
+    // CUDA graph of execute() for a fixed (in, out) pair: captured on a
+    // private stream, replayed into the caller's stream (cudaGraphLaunch)
+    bool use_graph;
+    cudaStream_t cap_stream;
+    cudaGraphExec_t gexec;
+    const void *g_in;
+    void *g_out;
+    int g_launches;
 };
 
 // Points staged per batch by the plane-owned 3D SM spread (nk_spread.cu).

@@ -302,6 +302,10 @@ class TransformPlan:
         k2 = "deconv" if self.type == 1 else "pad"
         return {k0: ms[0], "fft": ms[1], k2: ms[2], "total": ms[3]}
 
+    def set_timing(self, on):
+        """Per-stage CUDA-event timing (disables CUDA-graph replay while on)."""
+        _lib.check(self._lib.nk_set_timing(self._h, 1 if on else 0))
+
     def last_launch_count(self):
         return int(self._lib.nk_last_launch_count(self._h))
 

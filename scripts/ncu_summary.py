@@ -40,6 +40,16 @@ def run(rep):
         if k in h:
             i = h.index(k)
             print(f"  {k:<58} {vals[i]:>16} {units[i]}")
+    pipes = []
+    for k, v in zip(h, vals):
+        if k.startswith("sm__inst_executed_pipe_") and k.endswith("pct_of_peak_sustained_active"):
+            try:
+                pipes.append((float(v.replace(",", "")), k))
+            except ValueError:
+                pass
+    pipes.sort(reverse=True)
+    for v, k in pipes[:6]:
+        print(f"  pipe {k:<70} {v:>8.1f} %")
     stalls = [(k, v) for k, v in zip(h, vals) if k.startswith("smsp__average_warp_latency_issue_stalled_")
               or k.startswith("smsp__pcsamp_warps_issue_stalled_")]
     st = []

@@ -235,10 +235,20 @@ def run_ours(args, cfg):
     grid, pts, f_host, c_host = make_inputs(cfg, args.seed, rank)
     types = [2, 1] if cfg["type"] == 12 else [cfg["type"]]
     plans = {}
+    pts_dev = torch.from_numpy(pts).to(dev)
+    setpts_ms = {}
     for t in types:
         method = args.method or "default"
         plans[t] = nk.make_plan(t, cfg["modes"], cfg["eps"], method, cfg["prec"])
-        plans[t].set_points(torch.from_numpy(pts).to(dev))
+        plans[t].set_points(pts_dev)          # first call allocates
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        plans[t].set_points(pts_dev)          # setpts on resident coordinates
+        e1.record()
+        torch.cuda.synchronize()
+        setpts_ms[f"type{t}"] = e0.elapsed_time(e1)
     torch.cuda.synchronize()
     f_dev = torch.from_numpy(f_host).to(dev)
     c_dev = torch.from_numpy(c_host).to(dev)
@@ -421,6 +431,7 @@ def run_ours(args, cfg):
                                        "NCCL-reduced / type-2 modes NCCL-broadcast"
                                        if sharded else f"{world} independent replicas")},
             "gpu_launches": launches,
+            "setpts_ms": setpts_ms,
         }
         if dom_avg:
             B = algorithmic_bytes(cfg, fine)

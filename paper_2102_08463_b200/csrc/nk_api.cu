@@ -195,7 +195,8 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     // interpolation (one padded-bin load per bin).  Stage-level
     // build_subproblems keeps the reference default.
     p->msub = opts.max_subproblem ? opts.max_subproblem
-                                  : (type == 2 ? 4096 : (dim == 2 ? 256 : 1024));
+                                  : (type == 2 ? 4096
+                                               : (dim == 2 ? 256 : 1024));
     if (p->msub < 1) {
         nk_set_error("max subproblem size must be >= 1, got " + std::to_string(p->msub));
         delete p;

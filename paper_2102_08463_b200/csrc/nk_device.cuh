@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "nk_es_poly.h"
 #include "nk_internal.cuh"
 
 // binsort.py:98-100 grid_coords with numpy remainder semantics, bit-exact:
@@ -60,13 +61,46 @@ template <> __device__ __forceinline__ double nk_ceil<double>(double x) { return
 // Kernel row for one axis: local coordinate u (relative to the bin corner),
 // returns the local start cell ceil(u - w/2) (_kernels.py:43-46) and fills
 // ker[r] = phi((start + r - u) * 2/w) (_kernels.py:29-33).
+// Single precision: the interior pieces r = 1..w-2 are Horner polynomials in
+// s = 2 (start - u) + w - 1 with compile-time coefficients (nk_es_poly.h,
+// FFMA with immediate operands, no MUFU); the two edge pieces, which touch
+// the sqrt branch point at z = -1 / +1, keep the exact exp/sqrt path.
 template <typename T, int W>
 __device__ __forceinline__ int nk_kernel_row(T u, const Geom &g, T *ker) {
     const T st = nk_ceil<T>(u - (T)(0.5 * W));
-    const T z0 = (st - u) * (T)(2.0 / W);
+    if constexpr (sizeof(T) == 4 && W >= 3) {
+        const float d = st - u;
+        const float z0 = d * (2.0f / W);
+        ker[0] = nk_es(z0, g);
+        ker[W - 1] = nk_es(z0 + (float)(2.0 * (W - 1) / W), g);
+        const float s = fmaf(2.0f, d, (float)(W - 1));
+        typedef EsPoly<W> P;
 #pragma unroll
-    for (int r = 0; r < W; ++r) ker[r] = nk_es(z0 + (T)(2.0 * r / W), g);
+        for (int r = 1; r < W - 1; ++r) {
+            float p = P::c(r - 1, P::D);
+#pragma unroll
+            for (int k = P::D - 1; k >= 0; --k) p = fmaf(p, s, P::c(r - 1, k));
+            ker[r] = p;
+        }
+    } else {
+        const T z0 = (st - u) * (T)(2.0 / W);
+#pragma unroll
+        for (int r = 0; r < W; ++r) ker[r] = nk_es(z0 + (T)(2.0 * r / W), g);
+    }
     return (int)st;
+}
+
+// Packed single-precision FMA (sm_100 FFMA2): (a.x, a.y) * b + (c.x, c.y).
+__device__ __forceinline__ float2 nk_fma2(float2 a, float b, float2 c) {
+    unsigned long long r;
+    asm("{\n\t.reg .b64 bb;\n\tmov.b64 bb, {%2, %2};\n\tfma.rn.f32x2 %0, %1, bb, %3;\n\t}"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<unsigned long long *>(&a)), "f"(b),
+          "l"(*reinterpret_cast<unsigned long long *>(&c)));
+    return *reinterpret_cast<float2 *>(&r);
+}
+__device__ __forceinline__ double2 nk_fma2(double2 a, double b, double2 c) {
+    return make_double2(fma(a.x, b, c.x), fma(a.y, b, c.y));
 }
 
 __device__ __forceinline__ int nk_wrap(int l, int n) {
@@ -124,3 +158,20 @@ struct nk_divmod {
         : d(dd), magic((unsigned)((0x100000000ull + dd - 1) / dd)) {}
     __device__ __forceinline__ unsigned div(unsigned i) const { return __umulhi(i, magic); }
 };
+
+// Ampere-style asynchronous global -> shared copies (LDGSTS): no register
+// staging, completion tracked per commit group.
+__device__ __forceinline__ void nk_cp_async(float2 *smem, const float2 *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void nk_cp_async(double2 *smem, const double2 *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void nk_cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N> __device__ __forceinline__ void nk_cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}

@@ -7,6 +7,8 @@
 //  K7s staged ("sm" for type 2): one CTA per subproblem copies its padded
 //      bin (with periodic wrap) from HBM into shared memory once, then its
 //      points gather from shared memory.  Same per-point arithmetic.
+#include <algorithm>
+
 #include "nk_device.cuh"
 
 namespace {
@@ -76,19 +78,15 @@ k_interp_gm(int M, const int32_t *__restrict__ perm, const int32_t *__restrict__
     out[dst] = gather_global<T, D, W>(fine, g, s1, s2, s3, k1, k2, u3, st3);
 }
 
-template <typename T, int D, int W>
-__global__ void __launch_bounds__(256)
-k_interp_staged(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
-                const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
-                const T *__restrict__ pts, int64_t pitch,
-                const typename cplx<T>::t *__restrict__ fine, Geom g,
-                typename cplx<T>::t *__restrict__ out) {
-    typedef typename cplx<T>::t C;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    C *buf = reinterpret_cast<C *>(smem_raw);
-    const int s = blockIdx.x;
+// Copy subproblem s's padded bin (Eq. (16), periodic wrap) from the fine
+// grid into shared memory with cp.async (no register round trip; all of a
+// thread's copies are in flight at once).  Division-free index decode.
+template <typename T, int D>
+__device__ __forceinline__ void stage_padded_bin(typename cplx<T>::t *buf,
+                                                 const typename cplx<T>::t *__restrict__ fine,
+                                                 const Geom &g, int key) {
     int corner[3];
-    nk_bin_corner(sub_bin[s], g, corner);
+    nk_bin_corner(key, g, corner);
     const int h = g.halo;
     const int p1 = min(g.m[0], g.n[0] - corner[0]) + 2 * h;
     const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
@@ -104,69 +102,111 @@ k_interp_staged(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__
         int64_t l = nk_wrap(o1 + q1, g.n[0]) +
                     (int64_t)g.n[0] * (nk_wrap(o2 + q2, g.n[1]) +
                                        (D == 3 ? (int64_t)g.n[1] * nk_wrap(o3 + q3, g.n[2]) : 0));
-        buf[i] = __ldg(fine + l);
+        nk_cp_async(buf + i, fine + l);
     }
-    __syncthreads();
-    const int j0 = sub_start[s], j1 = sub_stop[s];
+}
+
+// K7s: persistent CTAs stride over the subproblems.  With NBUF = 2 the next
+// subproblem's padded bin streams into the second shared-memory buffer
+// (cp.async group) while the points of the current one gather, so the HBM
+// latency of the staging is hidden behind the gather arithmetic.  Points
+// are visited in footprint-start order (K4c), so a warp's 32 gathers from
+// one padded-bin row hit adjacent words (one shared-memory wavefront).
+template <typename T, int D, int W, int NBUF>
+__global__ void __launch_bounds__(256)
+k_interp_staged(int S, const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
+                const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
+                const T *__restrict__ pts, int64_t pitch,
+                const typename cplx<T>::t *__restrict__ fine, Geom g,
+                typename cplx<T>::t *__restrict__ out, int buf_cells) {
+    typedef typename cplx<T>::t C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *bufs = reinterpret_cast<C *>(smem_raw);
+    const int h = g.halo;
     const uint64_t keep = nk_policy_evict_last();
-    // software pipeline: the next point's coordinates and slot load while
-    // this point gathers
-    int j = j0 + threadIdx.x;
-    T u1n = 0, u2n = 0, u3n = 0;
-    int dstn = 0;
-    if (j < j1) {
-        u1n = __ldcs(pts + j);
-        u2n = __ldcs(pts + pitch + j);
-        if (D == 3) u3n = __ldcs(pts + 2 * pitch + j);
-        dstn = __ldcs(perm + j);
-    }
-    for (; j < j1; j += blockDim.x) {
-        const T u1 = u1n, u2 = u2n, u3 = u3n;
-        const int dst = dstn;
-        const int jn = j + blockDim.x;
-        if (jn < j1) {
-            u1n = __ldcs(pts + jn);
-            u2n = __ldcs(pts + pitch + jn);
-            if (D == 3) u3n = __ldcs(pts + 2 * pitch + jn);
-            dstn = __ldcs(perm + jn);
+    int s = blockIdx.x;
+    int cur = 0;
+    if (s < S) stage_padded_bin<T, D>(bufs, fine, g, sub_bin[s]);
+    nk_cp_async_commit();
+    for (; s < S; s += gridDim.x) {
+        const int sn = s + gridDim.x;
+        if (NBUF == 2) {
+            if (sn < S) stage_padded_bin<T, D>(bufs + (cur ^ 1) * buf_cells, fine, g, sub_bin[sn]);
+            nk_cp_async_commit();
+            nk_cp_async_wait<1>();
+        } else {
+            nk_cp_async_wait<0>();
         }
-        T k1[W], k2[W];
-        const int t1 = nk_kernel_row<T, W>(u1, g, k1) + h;
-        const int t2 = nk_kernel_row<T, W>(u2, g, k2) + h;
-        T st3 = 0;
-        if (D == 3) st3 = nk_ceil<T>(u3 - (T)(0.5 * W));
-        const int t3 = (int)st3 + (D == 3 ? h : 0);
-        T accr = 0, acci = 0;
+        __syncthreads();
+        const C *buf = bufs + cur * buf_cells;
+        int corner[3];
+        nk_bin_corner(sub_bin[s], g, corner);
+        const int p1 = min(g.m[0], g.n[0] - corner[0]) + 2 * h;
+        const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
+        const int j0 = sub_start[s], j1 = sub_stop[s];
+        // software pipeline: the next point's coordinates and output slot
+        // load while this point gathers
+        int j = j0 + threadIdx.x;
+        T u1n = 0, u2n = 0, u3n = 0;
+        int dstn = 0;
+        if (j < j1) {
+            u1n = __ldcs(pts + j);
+            u2n = __ldcs(pts + pitch + j);
+            if (D == 3) u3n = __ldcs(pts + 2 * pitch + j);
+            dstn = __ldcs(perm + j);
+        }
+        for (; j < j1; j += blockDim.x) {
+            const T u1 = u1n, u2 = u2n, u3 = u3n;
+            const int dst = dstn;
+            const int jn = j + blockDim.x;
+            if (jn < j1) {
+                u1n = __ldcs(pts + jn);
+                u2n = __ldcs(pts + pitch + jn);
+                if (D == 3) u3n = __ldcs(pts + 2 * pitch + jn);
+                dstn = __ldcs(perm + jn);
+            }
+            T k1[W], k2[W];
+            const int t1 = nk_kernel_row<T, W>(u1, g, k1) + h;
+            const int t2 = nk_kernel_row<T, W>(u2, g, k2) + h;
+            T st3 = 0;
+            if (D == 3) st3 = nk_ceil<T>(u3 - (T)(0.5 * W));
+            const int t3 = (int)st3 + (D == 3 ? h : 0);
+            C acc;
+            acc.x = 0;
+            acc.y = 0;
 #pragma unroll 1
-        for (int e = 0; e < (D == 3 ? W : 1); ++e) {
-            T mr = 0, mi = 0;
+            for (int e = 0; e < (D == 3 ? W : 1); ++e) {
+                C m;
+                m.x = 0;
+                m.y = 0;
 #pragma unroll
-            for (int b = 0; b < W; ++b) {
-                const C *row = buf + ((t3 + e) * p2 + (t2 + b)) * p1 + t1;
-                T ir = 0, ii = 0;
+                for (int b = 0; b < W; ++b) {
+                    const C *row = buf + ((t3 + e) * p2 + (t2 + b)) * p1 + t1;
+                    C ir;
+                    ir.x = 0;
+                    ir.y = 0;
 #pragma unroll
-                for (int a = 0; a < W; ++a) {
-                    C v = row[a];
-                    ir += v.x * k1[a];
-                    ii += v.y * k1[a];
+                    for (int a = 0; a < W; ++a) ir = nk_fma2(row[a], k1[a], ir);
+                    m = nk_fma2(ir, k2[b], m);
                 }
-                mr += ir * k2[b];
-                mi += ii * k2[b];
+                if (D == 3) {
+                    const T k3 = nk_es((st3 + (T)e - u3) * (T)(2.0 / W), g);
+                    acc = nk_fma2(m, k3, acc);
+                } else {
+                    acc = m;
+                }
             }
-            if (D == 3) {
-                const T k3 = nk_es((st3 + (T)e - u3) * (T)(2.0 / W), g);
-                accr += mr * k3;
-                acci += mi * k3;
-            } else {
-                accr = mr;
-                acci = mi;
-            }
+            nk_st_keep(out + dst, acc, keep);
         }
-        C o;
-        o.x = accr;
-        o.y = acci;
-        nk_st_keep(out + dst, o, keep);
+        __syncthreads();   // buffer cur is free for the prefetch after next
+        if (NBUF == 2) {
+            cur ^= 1;
+        } else if (sn < S) {
+            stage_padded_bin<T, D>(bufs, fine, g, sub_bin[sn]);
+            nk_cp_async_commit();
+        }
     }
+    nk_cp_async_wait<0>();
 }
 
 template <typename T, int D, int W>
@@ -176,14 +216,22 @@ int launch_w(nk_plan *p, const void *fine, void *out, int *launches) {
     if (M == 0) return NK_OK;
     if (p->method == NK_SM) {
         if (p->S == 0) return NK_OK;
-        size_t smem = (size_t)p->max_sub_smem;
-        auto kern = k_interp_staged<T, D, W>;
+        int nsm = 0;
+        NK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device));
+        const size_t one = (size_t)p->max_sub_smem;   // padded bin, 16-B rounded
+        // double-buffer when two padded bins leave room for a useful occupancy
+        const bool two = 2 * one <= 100 * 1024;
+        const size_t smem = two ? 2 * one : one;
+        auto kern = two ? k_interp_staged<T, D, W, 2> : k_interp_staged<T, D, W, 1>;
         NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-        kern<<<(unsigned)p->S, 256, smem, p->stream>>>(p->d_sub_bin, p->d_sub_start,
-                                                      p->d_sub_stop, p->d_vperm,
-                                                      (const T *)p->d_pts, p->cap_M,
-                                                      (const C *)fine, p->geom, (C *)out);
+        int per_sm = 0;
+        NK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+        const int64_t grid = std::min<int64_t>(p->S, (int64_t)std::max(per_sm, 1) * nsm);
+        kern<<<(unsigned)grid, 256, smem, p->stream>>>(
+            (int)p->S, p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm,
+            (const T *)p->d_pts, p->cap_M, (const C *)fine, p->geom, (C *)out,
+            (int)(one / sizeof(C)));
     } else {
         const int32_t *perm = p->method == NK_GM ? nullptr : p->d_vperm;
         k_interp_gm<T, D, W><<<(M + 255) / 256, 256, 0, p->stream>>>(

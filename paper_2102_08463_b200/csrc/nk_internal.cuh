@@ -122,6 +122,10 @@ struct nk_plan {
     int g_launches;
 };
 
+// Warps per CTA of the plane-owned 3D SM spread (nk_spread.cu): warp w owns
+// padded-bin planes z == w (mod NW), ceil(w / NW) planes per footprint.  4
+// measured fastest for w <= 8 (C3: 1.87 ms vs 2.35 ms with 8, 2.38 with 2).
+constexpr int nk_sm3_warps(int w) { return w <= 8 ? 4 : 16; }
 // Points staged per batch by the plane-owned 3D SM spread (nk_spread.cu).
 inline int nk_sm3_batch(int prec) { return prec == NK_DOUBLE ? 64 : 128; }
 // Dynamic shared memory (bytes) of the SM spread / staged interp for a plan

@@ -443,6 +443,46 @@ k_start_sort(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     }
 }
 
+// ---------------------------------------------------------------- K4d
+// Type-1 visit order (bin, footprint start): start offset of every point in
+// its bin's padded frame, from the visit-order local coordinates (the same
+// T-precision ceil the spread kernel evaluates).
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_start_keys(int M, const int32_t *__restrict__ bin_keys, const T *__restrict__ pts,
+             int64_t pitch, Geom g, int32_t *__restrict__ skeys) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= M) return;
+    int corner[3];
+    nk_bin_corner(bin_keys[j], g, corner);
+    const int h = g.halo;
+    const int p1 = min(g.m[0], g.n[0] - corner[0]) + 2 * h;
+    const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
+    const T half = (T)(0.5 * g.w);
+    const int t1 = (int)nk_ceil<T>(pts[j] - half) + h;
+    const int t2 = (int)nk_ceil<T>(pts[pitch + j] - half) + h;
+    const int t3 = g.dim == 3 ? (int)nk_ceil<T>(pts[2 * pitch + j] - half) + h : 0;
+    skeys[j] = (t3 * p2 + t2) * p1 + t1;
+}
+
+__global__ void k_gather_i32(int M, const int32_t *__restrict__ idx,
+                             const int32_t *__restrict__ src, int32_t *__restrict__ dst) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < M) dst[i] = src[idx[i]];
+}
+
+template <typename T>
+__global__ void k_reorder_points(int M, int dim, const int32_t *__restrict__ q,
+                                 const int32_t *__restrict__ perm_in, const T *__restrict__ pts_in,
+                                 int64_t pitch, int32_t *__restrict__ perm_out,
+                                 T *__restrict__ pts_out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const int src = q[i];
+    perm_out[i] = perm_in[src];
+    for (int a = 0; a < dim; ++a) pts_out[a * pitch + i] = pts_in[a * pitch + src];
+}
+
 template <typename T>
 int grow(T **ptr, int64_t *cap, int64_t need) {
     if (need <= *cap && *ptr) return NK_OK;
@@ -491,7 +531,7 @@ static int ensure_point_buffers(nk_plan *p, int64_t M) {
     NK_CUDA(cudaMalloc((void **)&p->d_alt_keys, 4 * n));
     NK_CUDA(cudaMalloc((void **)&p->d_alt_vals, 4 * n));
     NK_CUDA(cudaMalloc(&p->d_pts, (size_t)p->csize / 2 * p->dim * n));
-    if (p->type == 2 && p->method == NK_SM) {
+    if (p->method == NK_SM) {
         NK_CUDA(cudaMalloc((void **)&p->d_vperm_buf, 4 * n));
         NK_CUDA(cudaMalloc(&p->d_pts_alt, (size_t)p->csize / 2 * p->dim * n));
     }
@@ -517,6 +557,88 @@ static int gather(nk_plan *p, const int32_t *perm, const void *x, const void *y,
         M, perm, (const TC *)x, (const TC *)y, (const TC *)z, stride, p->geom, (T *)p->d_pts,
         p->cap_M);
     NK_LAUNCH_CHECK();
+    return NK_OK;
+}
+
+// Stable LSD radix sort of (key, value) pairs on the low `bits` bits of
+// the keys; vin == nullptr means values = positions.  The last pass lands
+// in (out_k, out_v); (tmp_k, tmp_v) is the ping-pong scratch.  Inputs are
+// read by the first pass only.
+static int radix_sort_pairs(nk_plan *p, const int32_t *kin, const int32_t *vin, int64_t M,
+                            int bits, int32_t *out_k, int32_t *out_v, int32_t *tmp_k,
+                            int32_t *tmp_v) {
+    cudaStream_t st = p->stream;
+    const int passes = std::max(1, (bits + RADIX_BITS - 1) / RADIX_BITS);
+    const int ntiles = (int)((M + SORT_TILE - 1) / SORT_TILE);
+    int rc = grow(&p->d_tile_hist, &p->cap_tile_hist, (int64_t)RADIX * ntiles + 1);
+    if (rc) return rc;
+    int32_t *A[2] = {out_k, out_v}, *B[2] = {tmp_k, tmp_v};
+    for (int ps = 0; ps < passes; ++ps) {
+        const bool toA = ((passes - 1 - ps) % 2) == 0;   // the last pass lands in A
+        int32_t **dst = toA ? A : B;
+        const int shift = ps * RADIX_BITS;
+        k_radix_hist<<<ntiles, SORT_BLOCK, 0, st>>>(kin, (int)M, shift, ntiles, p->d_tile_hist);
+        NK_LAUNCH_CHECK();
+        rc = nk_scan_exclusive(p, p->d_tile_hist, p->d_tile_hist, (int64_t)RADIX * ntiles);
+        if (rc) return rc;
+        k_radix_scatter<<<ntiles, SORT_BLOCK, 0, st>>>(kin, vin, (int)M, shift, ntiles,
+                                                       p->d_tile_hist, dst[0], dst[1]);
+        NK_LAUNCH_CHECK();
+        kin = dst[0];
+        vin = dst[1];
+    }
+    return NK_OK;
+}
+
+static int bits_for(int64_t n) {
+    int b = 1;
+    while ((1ll << b) < n) ++b;
+    return b;
+}
+
+// Type-1 SM visit order: stable by (bin, footprint start), so points that
+// share a footprint are adjacent across the whole bin and the spread can
+// accumulate them in registers (nk_spread.cu).  Two stable LSD sorts: by
+// start, then by bin key.  The exported bin-stable layout (d_perm) stays.
+static int order_by_start(nk_plan *p) {
+    const int64_t M = p->M;
+    cudaStream_t st = p->stream;
+    int32_t *scr = nullptr;
+    NK_CUDA(cudaMalloc((void **)&scr, 4 * 4 * (size_t)M));
+    int32_t *k0 = scr, *v0 = scr + M, *k1 = scr + 2 * M, *v1 = scr + 3 * M;
+    const unsigned nb = blocks_for(M, 256);
+    if (p->prec == NK_DOUBLE)
+        k_start_keys<double><<<nb, 256, 0, st>>>((int)M, p->d_keys, (const double *)p->d_pts,
+                                                 p->cap_M, p->geom, k0);
+    else
+        k_start_keys<float><<<nb, 256, 0, st>>>((int)M, p->d_keys, (const float *)p->d_pts,
+                                                p->cap_M, p->geom, k0);
+    int rc = radix_sort_pairs(p, k0, nullptr, M, bits_for(p->max_pad_cells), p->d_alt_keys,
+                              p->d_alt_vals, k1, v1);
+    if (!rc) {
+        k_gather_i32<<<nb, 256, 0, st>>>((int)M, p->d_alt_vals, p->d_keys, k0);
+        rc = radix_sort_pairs(p, k0, p->d_alt_vals, M, bits_for(p->nbins), p->d_alt_keys, v0,
+                              k1, v1);
+    }
+    if (!rc) {
+        if (p->prec == NK_DOUBLE)
+            k_reorder_points<double><<<nb, 256, 0, st>>>(
+                (int)M, p->dim, v0, p->d_perm, (const double *)p->d_pts, p->cap_M,
+                p->d_vperm_buf, (double *)p->d_pts_alt);
+        else
+            k_reorder_points<float><<<nb, 256, 0, st>>>(
+                (int)M, p->dim, v0, p->d_perm, (const float *)p->d_pts, p->cap_M,
+                p->d_vperm_buf, (float *)p->d_pts_alt);
+        std::swap(p->d_pts, p->d_pts_alt);
+        p->d_vperm = p->d_vperm_buf;
+    }
+    cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(scr);
+    if (rc) return rc;
+    if (e != cudaSuccess) {
+        nk_set_error(std::string("CUDA error: ") + cudaGetErrorString(e));
+        return NK_ERR_CUDA;
+    }
     return NK_OK;
 }
 
@@ -549,29 +671,9 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
     const int32_t *perm = nullptr;
     p->sorted = false;
     if (p->method != NK_GM && M > 0) {
-        int bits = 1;
-        while ((1ll << bits) < p->nbins) ++bits;
-        int passes = (bits + RADIX_BITS - 1) / RADIX_BITS;
-        int ntiles = (int)((M + SORT_TILE - 1) / SORT_TILE);
-        rc = grow(&p->d_tile_hist, &p->cap_tile_hist, (int64_t)RADIX * ntiles + 1);
+        rc = radix_sort_pairs(p, p->d_keys_in, nullptr, M, bits_for(p->nbins), p->d_keys,
+                              p->d_perm, p->d_alt_keys, p->d_alt_vals);
         if (rc) return rc;
-        int32_t *A[2] = {p->d_keys, p->d_perm}, *B[2] = {p->d_alt_keys, p->d_alt_vals};
-        const int32_t *kin = p->d_keys_in, *vin = nullptr;
-        for (int ps = 0; ps < passes; ++ps) {
-            bool toA = ((passes - 1 - ps) % 2) == 0;   // the last pass lands in A
-            int32_t **dst = toA ? A : B;
-            int shift = ps * RADIX_BITS;
-            k_radix_hist<<<ntiles, SORT_BLOCK, 0, st>>>(kin, (int)M, shift, ntiles,
-                                                        p->d_tile_hist);
-            NK_LAUNCH_CHECK();
-            rc = nk_scan_exclusive(p, p->d_tile_hist, p->d_tile_hist, (int64_t)RADIX * ntiles);
-            if (rc) return rc;
-            k_radix_scatter<<<ntiles, SORT_BLOCK, 0, st>>>(kin, vin, (int)M, shift, ntiles,
-                                                           p->d_tile_hist, dst[0], dst[1]);
-            NK_LAUNCH_CHECK();
-            kin = dst[0];
-            vin = dst[1];
-        }
         perm = p->d_perm;
         p->sorted = true;
     } else if (M > 0) {
@@ -618,6 +720,10 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
         }
     }
     p->d_vperm = p->d_perm;
+    if (p->type == 1 && p->method == NK_SM && p->dim == 3 && p->S > 0) {
+        rc = order_by_start(p);
+        if (rc) return rc;
+    }
     if (p->type == 2 && p->method == NK_SM && p->S > 0) {
         // single precision: footprint-start order (one wavefront per warp
         // gather row); double: bank-residue interleave (16-byte cells, 3D

@@ -58,23 +58,28 @@ k_spread_gm(int M, const int32_t *__restrict__ perm, const int32_t *__restrict__
     }
 }
 
-// K6c-3D: plane-owned shared-memory spreading, no atomics.  A CTA owns one
-// subproblem's padded bin (p1 x p2 x p3 cells, Eq. (16)).  Points are
-// staged in batches: each thread evaluates one point's three kernel rows
-// (c folded into the axis-3 row) into shared memory.  Then every warp walks
-// the whole batch, but warp w only updates the padded-bin planes
-// z == w (mod 8): planes are owned, lanes cover distinct (a, b) cells of a
+// K6c-3D: plane-owned shared-memory spreading with run accumulation, no
+// atomics.  A CTA of NW warps owns one subproblem's padded bin (p1 x p2 x
+// p3 cells, Eq. (16)).  Points are staged in batches: each thread evaluates
+// one point's three kernel rows (c folded into the axis-3 row) into shared
+// memory.  Every warp walks the whole batch; warp w only touches padded-bin
+// planes z == w (mod NW), its lanes covering distinct (a, b) cells of a
 // plane, so plain read-modify-write replaces the CAS loops that
-// atomicAdd(float/double) compiles to on shared memory.  The finished bin is
-// merged with native global vector reductions (Eq. (17)).
-template <typename T, int W>
-__global__ void __launch_bounds__(256)
+// atomicAdd(float/double) compiles to on shared memory.  Points arrive in
+// (bin, footprint start) order (setpts K4d); while the start stays the same
+// a lane keeps its cells' sums in registers and writes them to shared memory
+// only when the start changes (clustered points: one read-modify-write per
+// run instead of per point).  The finished bin is merged with native global
+// vector reductions (Eq. (17)).
+template <typename T, int W, int NW>
+__global__ void __launch_bounds__(NW * 32)
 k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
              const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
              const T *__restrict__ pts, int64_t pitch, const typename cplx<T>::t *__restrict__ c,
              Geom g, typename cplx<T>::t *__restrict__ fine, int64_t stage_off, int nbatch) {
     typedef typename cplx<T>::t C;
     constexpr int NIT = (W * W + 31) / 32;
+    constexpr int NE = (W + NW - 1) / NW;   // planes per warp per footprint
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *buf = reinterpret_cast<C *>(smem_raw);
     int2 *sst = reinterpret_cast<int2 *>(smem_raw + stage_off);
@@ -106,6 +111,33 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
         zero.y = 0;
         buf[i] = zero;
     }
+    C acc[NE][NIT];
+#pragma unroll
+    for (int k = 0; k < NE; ++k)
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) acc[k][it].x = acc[k][it].y = 0;
+    int run_off = -1, e0 = 0;
+    // add the register sums of the current run to its planes, then clear
+    auto flush = [&]() {
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            const int e = e0 + k * NW;
+            if (e < W) {
+                C *plane = buf + run_off + e * pstride;
+#pragma unroll
+                for (int it = 0; it < NIT; ++it) {
+                    if (it < NIT - 1 || last_ok) {
+                        C *cell = plane + lofs[it];
+                        C v = *cell;
+                        v.x += acc[k][it].x;
+                        v.y += acc[k][it].y;
+                        *cell = v;
+                    }
+                    acc[k][it].x = acc[k][it].y = 0;
+                }
+            }
+        }
+    };
     const int j0 = sub_start[s], j1 = sub_stop[s];
     for (int base = j0; base < j1; base += nbatch) {
         const int nb = min(nbatch, j1 - base);
@@ -131,71 +163,30 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
             sst[q] = make_int2((t3 * p2 + t2) * p1 + t1, t3);
         }
         __syncthreads();
-        if (W <= 8) {
-            // at most one owned plane per point: software-pipelined so the
-            // next point's staged values load while this point's cells are
-            // read-modified-written
-            int2 st = sst[0];
-            int e = (warp - st.y) & 7;
-            C ck = sck3[min(e, W - 1)];
+        for (int q = 0; q < nb; ++q) {
+            const int2 st = sst[q];
+            if (st.x != run_off) {   // uniform across the CTA
+                if (run_off >= 0) flush();
+                run_off = st.x;
+                e0 = (warp - st.y) & (NW - 1);
+            }
+            const T *k1q = sk1 + q * W;
+            const T *k2q = sk2 + q * W;
             T kk[NIT];
 #pragma unroll
-            for (int it = 0; it < NIT; ++it) kk[it] = sk2[lb[it]] * sk1[la[it]];
-            for (int q = 0; q < nb; ++q) {
-                const int qn = min(q + 1, nb - 1);
-                const int2 stn = sst[qn];
-                const int en = (warp - stn.y) & 7;
-                const C ckn = sck3[qn * W + min(en, W - 1)];
-                T kkn[NIT];
+            for (int it = 0; it < NIT; ++it) kk[it] = k2q[lb[it]] * k1q[la[it]];
 #pragma unroll
-                for (int it = 0; it < NIT; ++it) kkn[it] = sk2[qn * W + lb[it]] * sk1[qn * W + la[it]];
+            for (int k = 0; k < NE; ++k) {
+                const int e = e0 + k * NW;
                 if (e < W) {
-                    C *plane = buf + st.x + e * pstride;
-#pragma unroll
-                    for (int it = 0; it < NIT; ++it) {
-                        if (it < NIT - 1 || last_ok) {
-                            C *cell = plane + lofs[it];
-                            C v = *cell;
-                            v.x += ck.x * kk[it];
-                            v.y += ck.y * kk[it];
-                            *cell = v;
-                        }
-                    }
-                }
-                __syncwarp();
-                st = stn;
-                e = en;
-                ck = ckn;
-#pragma unroll
-                for (int it = 0; it < NIT; ++it) kk[it] = kkn[it];
-            }
-        } else {
-            for (int q = 0; q < nb; ++q) {
-                const int2 st = sst[q];
-                const T *k1q = sk1 + q * W;
-                const T *k2q = sk2 + q * W;
-                T kk[NIT];
-#pragma unroll
-                for (int it = 0; it < NIT; ++it) kk[it] = k2q[lb[it]] * k1q[la[it]];
-#pragma unroll 1
-                for (int e = (warp - st.y) & 7; e < W; e += 8) {
                     const C ck = sck3[q * W + e];
-                    C *plane = buf + st.x + e * pstride;
 #pragma unroll
-                    for (int it = 0; it < NIT; ++it) {
-                        if (it < NIT - 1 || last_ok) {
-                            C *cell = plane + lofs[it];
-                            C v = *cell;
-                            v.x += ck.x * kk[it];
-                            v.y += ck.y * kk[it];
-                            *cell = v;
-                        }
-                    }
+                    for (int it = 0; it < NIT; ++it) acc[k][it] = nk_fma2(ck, kk[it], acc[k][it]);
                 }
-                __syncwarp();
             }
         }
     }
+    if (run_off >= 0) flush();
     __syncthreads();
     const int o1 = corner[0] - h, o2 = corner[1] - h, o3 = corner[2] - h;
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
@@ -333,11 +324,12 @@ int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
     if (p->method == NK_SM && D == 3) {
         if (p->S == 0) return NK_OK;
         size_t smem = (size_t)p->max_sub_smem;
-        auto kern = k_spread_sm3<T, W>;
+        constexpr int NW = nk_sm3_warps(W);
+        auto kern = k_spread_sm3<T, W, NW>;
         NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         int64_t stage_off = (p->max_pad_cells * (int64_t)sizeof(C) + 15) / 16 * 16;
-        kern<<<(unsigned)p->S, 256, smem, p->stream>>>(
+        kern<<<(unsigned)p->S, NW * 32, smem, p->stream>>>(
             p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm, (const T *)p->d_pts,
             p->cap_M, (const C *)c, p->geom, (C *)fine, stage_off, nk_sm3_batch(p->prec));
     } else if (p->method == NK_SM && D == 2) {

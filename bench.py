@@ -42,6 +42,18 @@ CONFIGS = {
     "c3b": dict(type=1, modes=(128, 128, 128), M=10_000_000, dist="gauss", eps=1e-6,
                 prec="single",
                 desc="C3b 3D type-1 f32 N=128^3 M=1e7 Gaussian(0,(pi/8)^2) eps=1e-6"),
+    "c3t2": dict(type=2, modes=(128, 128, 128), M=10_000_000, dist="gauss", eps=1e-6,
+                 prec="single",
+                 desc="C3t2 3D type-2 f32 N=128^3 M=1e7 Gaussian(0,(pi/8)^2) eps=1e-6 "
+                      "(north_star 3D single type-2 target)"),
+    "c3t2u": dict(type=2, modes=(128, 128, 128), M=10_000_000, dist="rand", eps=1e-5,
+                  prec="single",
+                  desc="C3t2u 3D type-2 f32 N=128^3 M=1e7 uniform eps=1e-5 "
+                       "(north_star 3D single type-2 target)"),
+    "c3t1u": dict(type=1, modes=(128, 128, 128), M=10_000_000, dist="rand", eps=1e-5,
+                  prec="single",
+                  desc="C3t1u 3D type-1 f32 N=128^3 M=1e7 uniform eps=1e-5 "
+                       "(north_star 3D single type-1 target)"),
     "c4t1": dict(type=1, modes=(256, 256, 256), M=100_000_000, dist="rand", eps=1e-12,
                  prec="double", desc="C4 3D type-1 f64 N=256^3 M=1e8 uniform eps=1e-12"),
     "c4t2": dict(type=2, modes=(256, 256, 256), M=100_000_000, dist="rand", eps=1e-12,

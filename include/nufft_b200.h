@@ -65,6 +65,9 @@ typedef struct {
     int device;          /* -1 = current device */
     void *stream;        /* cudaStream_t, NULL = default stream */
     int timing;          /* nonzero: record per-stage CUDA events (nk_stage_times) */
+    int n_trans;         /* vectors per execute (cufinufft ntransf); 0 or 1 = one.  The
+                            reference has no batching; the paper reuses
+                            one setpts across many transforms */
 } nk_opts;
 
 typedef struct {
@@ -82,6 +85,7 @@ typedef struct {
     int halo;
     int64_t num_points;
     int64_t num_subproblems;
+    int n_trans;
 } nk_plan_info;
 
 /* ---- plan-time host math (kernel.py) --------------------------------- */
@@ -121,7 +125,9 @@ NK_API int nk_setpts(nk_plan *plan, int64_t M, int coord_prec, const void *x, co
               const void *z, int64_t stride);
 
 /* execute(plan, input, output): type 1 reads M strengths
- * and writes prod(N) modes; type 2 the reverse.  Input is not modified. */
+ * and writes prod(N) modes; type 2 the reverse.  Input is not modified.
+ * With n_trans = K > 1 the input and output hold K vectors back to back
+ * (type 1: K x M strengths -> K x prod(N) modes). */
 NK_API int nk_execute(nk_plan *plan, const void *in, void *out);
 
 /* destroy. */
@@ -144,7 +150,8 @@ NK_API int nk_get_subproblems(const nk_plan *plan, int32_t *bin_ids, int32_t *sl
                        int32_t *slice_stops, int32_t *offsets, int32_t *padded_dims);
 
 /* spread_gm / spread_gm_sort / spread_sm (spread.py:142-182): zero `fine`
- * then spread the M strengths with the plan method. */
+ * then spread the M strengths with the plan method.  Stage functions act on
+ * all n_trans vectors (buffers hold n_trans back-to-back arrays). */
 NK_API int nk_spread(nk_plan *plan, const void *strengths, void *fine);
 
 /* interpolate: out[j] = gather at point j. */

@@ -28,7 +28,7 @@ class NkOpts(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int), ("bin_dims", ctypes.c_int * 3),
                 ("max_subproblem", ctypes.c_int), ("fine", ctypes.c_int64 * 3),
                 ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
-                ("timing", ctypes.c_int)]
+                ("timing", ctypes.c_int), ("n_trans", ctypes.c_int)]
 
 
 class NkPlanInfo(ctypes.Structure):
@@ -40,7 +40,7 @@ class NkPlanInfo(ctypes.Structure):
                 ("bin_dims", ctypes.c_int * 3), ("bins_per_axis", ctypes.c_int64 * 3),
                 ("nbins", ctypes.c_int64), ("max_subproblem", ctypes.c_int),
                 ("halo", ctypes.c_int), ("num_points", ctypes.c_int64),
-                ("num_subproblems", ctypes.c_int64)]
+                ("num_subproblems", ctypes.c_int64), ("n_trans", ctypes.c_int)]
 
 
 class NufftError(RuntimeError):

@@ -105,6 +105,7 @@ extern "C" void nk_default_opts(nk_opts *o) {
     memset(o, 0, sizeof(*o));
     o->method = NK_METHOD_DEFAULT;
     o->device = -1;
+    o->n_trans = 1;
 }
 
 extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double eps, int precision,
@@ -139,8 +140,13 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
         return NK_ERR_VALUE;
     }
 
+    if (opts.n_trans < 0 || opts.n_trans > (1 << 20)) {
+        nk_set_error("n_trans must be >= 1, got " + std::to_string(opts.n_trans));
+        return NK_ERR_VALUE;
+    }
     nk_plan *p = new nk_plan();
     memset((void *)p, 0, sizeof(*p));
+    p->ntrans = opts.n_trans > 0 ? opts.n_trans : 1;
     p->type = type;
     p->dim = dim;
     p->prec = precision;
@@ -269,6 +275,9 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     g.beta = beta;
     g.betaf = (float)beta;
     g.betaf_log2e = (float)(beta * 1.4426950408889634);
+    g.ntot = p->n_tot;
+    g.Ntot = p->N_tot;
+    g.M = 0;
 
     // correction factors, per axis, with (2/w) and the (-1)^k phase folded in
     std::vector<double> corr;
@@ -302,7 +311,7 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
         nk_set_error(std::string("device allocation failed: ") + cudaGetErrorString(e)); \
         return fail(NK_ERR_MEMORY);                                                 \
     }
-    NK_ALLOC(p->d_fine, p->n_tot * p->csize);
+    NK_ALLOC(p->d_fine, p->n_tot * p->csize * p->ntrans);
     NK_ALLOC(p->d_corr, corr.size() * p->csize / 2);
     NK_ALLOC(p->d_counts, 4 * p->nbins);
     NK_ALLOC(p->d_starts, 4 * (p->nbins + 1));
@@ -323,8 +332,9 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     // cuFFT plan on the fine grid, slowest axis first
     int nn[3];
     for (int i = 0; i < dim; ++i) nn[i] = (int)p->n[dim - 1 - i];
-    cufftResult fr = cufftPlanMany(&p->fft, dim, nn, nullptr, 1, 0, nullptr, 1, 0,
-                                   precision == NK_DOUBLE ? CUFFT_Z2Z : CUFFT_C2C, 1);
+    cufftResult fr = cufftPlanMany(&p->fft, dim, nn, nn, 1, (int)p->n_tot, nn, 1,
+                                   (int)p->n_tot, precision == NK_DOUBLE ? CUFFT_Z2Z : CUFFT_C2C,
+                                   p->ntrans);
     if (fr != CUFFT_SUCCESS) {
         nk_set_error(std::string("cufftPlanMany failed: ") + cufft_msg(fr));
         return fail(fr == CUFFT_ALLOC_FAILED ? NK_ERR_MEMORY : NK_ERR_CUDA);
@@ -373,6 +383,7 @@ extern "C" int nk_plan_get_info(const nk_plan *p, nk_plan_info *info) {
     info->halo = p->halo;
     info->num_points = p->have_points ? p->M : 0;
     info->num_subproblems = p->S;
+    info->n_trans = p->ntrans;
     return NK_OK;
 }
 
@@ -405,6 +416,7 @@ extern "C" int nk_setpts(nk_plan *p, int64_t M, int coord_prec, const void *x, c
         }
     p->have_points = false;
     p->M = M;
+    p->geom.M = M;
     if (p->gexec) {   // kernel parameters (M, S, buffers) change with the points
         cudaGraphExecDestroy(p->gexec);
         p->gexec = nullptr;
@@ -520,8 +532,8 @@ extern "C" int nk_execute(nk_plan *p, const void *in, void *out) {
         nk_set_error("execute called before set_points");
         return NK_ERR_STATE;
     }
-    const size_t in_bytes = (p->type == 1 ? p->M : p->N_tot) * p->csize;
-    const size_t out_bytes = (p->type == 1 ? p->N_tot : p->M) * p->csize;
+    const size_t in_bytes = (p->type == 1 ? p->M : p->N_tot) * p->csize * p->ntrans;
+    const size_t out_bytes = (p->type == 1 ? p->N_tot : p->M) * p->csize * p->ntrans;
     if ((in_bytes && !in) || (out_bytes && !out)) {
         nk_set_error("null input or output buffer");
         return NK_ERR_VALUE;

@@ -20,6 +20,8 @@ k_deconv1(Geom g, const T *__restrict__ corr, const typename cplx<T>::t *__restr
     typedef typename cplx<T>::t C;
     const int N1 = g.N[0], N2 = g.N[1];
     const int row = blockIdx.x;            // i2 + N2 * i3
+    spec += blockIdx.y * g.ntot;           // batched execute: vector blockIdx.y
+    modes += blockIdx.y * g.Ntot;
     const int i2 = row % N2, i3 = row / N2;
     const int l2 = nk_wrap(i2 - N2 / 2, g.n[1]);
     T frow = corr[N1 + i2];
@@ -59,6 +61,8 @@ k_deconv2(Geom g, const T *__restrict__ corr, const typename cplx<T>::t *__restr
     const int n1 = g.n[0], n2 = g.n[1];
     const int N1 = g.N[0], N2 = g.N[1];
     const int row = blockIdx.x;            // l2 + n2 * l3
+    modes += blockIdx.y * g.Ntot;          // batched execute: vector blockIdx.y
+    spec += blockIdx.y * g.ntot;
     const int l2 = row % n2, l3 = row / n2;
     const int i2 = mode_of(l2, N2, n2);
     const int i3 = g.dim == 3 ? mode_of(l3, g.N[2], g.n[2]) : 0;
@@ -90,24 +94,24 @@ k_deconv2(Geom g, const T *__restrict__ corr, const typename cplx<T>::t *__restr
 
 int nk_launch_deconv1(nk_plan *p, const void *spec, void *modes) {
     if (p->N_tot == 0) return NK_OK;
-    unsigned rows = (unsigned)(p->N[1] * p->N[2]);
+    const dim3 grid((unsigned)(p->N[1] * p->N[2]), p->ntrans);
     if (p->prec == NK_DOUBLE)
-        k_deconv1<double><<<rows, 256, 0, p->stream>>>(p->geom, (const double *)p->d_corr,
+        k_deconv1<double><<<grid, 256, 0, p->stream>>>(p->geom, (const double *)p->d_corr,
                                                        (const double2 *)spec, (double2 *)modes);
     else
-        k_deconv1<float><<<rows, 256, 0, p->stream>>>(p->geom, (const float *)p->d_corr,
+        k_deconv1<float><<<grid, 256, 0, p->stream>>>(p->geom, (const float *)p->d_corr,
                                                       (const float2 *)spec, (float2 *)modes);
     NK_LAUNCH_CHECK();
     return NK_OK;
 }
 
 int nk_launch_deconv2(nk_plan *p, const void *modes, void *spec) {
-    unsigned rows = (unsigned)(p->n[1] * p->n[2]);
+    const dim3 grid((unsigned)(p->n[1] * p->n[2]), p->ntrans);
     if (p->prec == NK_DOUBLE)
-        k_deconv2<double><<<rows, 256, 0, p->stream>>>(p->geom, (const double *)p->d_corr,
+        k_deconv2<double><<<grid, 256, 0, p->stream>>>(p->geom, (const double *)p->d_corr,
                                                        (const double2 *)modes, (double2 *)spec);
     else
-        k_deconv2<float><<<rows, 256, 0, p->stream>>>(p->geom, (const float *)p->d_corr,
+        k_deconv2<float><<<grid, 256, 0, p->stream>>>(p->geom, (const float *)p->d_corr,
                                                       (const float2 *)modes, (float2 *)spec);
     NK_LAUNCH_CHECK();
     return NK_OK;

@@ -42,6 +42,10 @@ struct Geom {
     double scale[3];  // n_i / (2 pi), binsort.py:99
     float betaf, betaf_log2e;
     double beta;
+    // per-vector strides of a batched execute (vector = blockIdx.y)
+    int64_t ntot;   // fine cells
+    int64_t Ntot;   // modes
+    int64_t M;      // points
 };
 
 template <typename T> struct cplx;
@@ -51,6 +55,7 @@ template <> struct cplx<double> { typedef double2 t; };
 // -------------------------------------------------------------- plan
 struct nk_plan {
     int type, dim, prec, method;
+    int ntrans;     // vectors per execute (cufinufft ntransf), >= 1
     int64_t N[3], n[3];
     double eps;
     int w;

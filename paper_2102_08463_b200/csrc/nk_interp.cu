@@ -63,6 +63,8 @@ k_interp_gm(int M, const int32_t *__restrict__ perm, const int32_t *__restrict__
             typename cplx<T>::t *__restrict__ out) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= M) return;
+    fine += blockIdx.y * g.ntot;   // batched execute: vector blockIdx.y
+    out += blockIdx.y * g.M;
     int corner[3];
     nk_bin_corner(keys[j], g, corner);
     T k1[W], k2[W];
@@ -124,6 +126,8 @@ k_interp_staged(int S, const int32_t *__restrict__ sub_bin, const int32_t *__res
     C *bufs = reinterpret_cast<C *>(smem_raw);
     const int h = g.halo;
     const uint64_t keep = nk_policy_evict_last();
+    fine += blockIdx.y * g.ntot;   // batched execute: vector blockIdx.y
+    out += blockIdx.y * g.M;
     int s = blockIdx.x;
     int cur = 0;
     if (s < S) stage_padded_bin<T, D>(bufs, fine, g, sub_bin[s]);
@@ -228,13 +232,13 @@ int launch_w(nk_plan *p, const void *fine, void *out, int *launches) {
         int per_sm = 0;
         NK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
         const int64_t grid = std::min<int64_t>(p->S, (int64_t)std::max(per_sm, 1) * nsm);
-        kern<<<(unsigned)grid, 256, smem, p->stream>>>(
+        kern<<<dim3((unsigned)grid, p->ntrans), 256, smem, p->stream>>>(
             (int)p->S, p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm,
             (const T *)p->d_pts, p->cap_M, (const C *)fine, p->geom, (C *)out,
             (int)(one / sizeof(C)));
     } else {
         const int32_t *perm = p->method == NK_GM ? nullptr : p->d_vperm;
-        k_interp_gm<T, D, W><<<(M + 255) / 256, 256, 0, p->stream>>>(
+        k_interp_gm<T, D, W><<<dim3((M + 255) / 256, p->ntrans), 256, 0, p->stream>>>(
             M, perm, p->d_keys, (const T *)p->d_pts, p->cap_M, (const C *)fine, p->geom,
             (C *)out);
     }

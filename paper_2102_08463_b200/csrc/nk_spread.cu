@@ -19,6 +19,8 @@ k_spread_gm(int M, const int32_t *__restrict__ perm, const int32_t *__restrict__
     typedef typename cplx<T>::t C;
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= M) return;
+    c += blockIdx.y * g.M;
+    fine += blockIdx.y * g.ntot;
     int corner[3];
     nk_bin_corner(keys[j], g, corner);
     const int src = perm ? perm[j] : j;
@@ -88,6 +90,8 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     C *sck3 = reinterpret_cast<C *>(sk2 + nbatch * W);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x;
+    c += blockIdx.y * g.M;          // batched execute: vector blockIdx.y
+    fine += blockIdx.y * g.ntot;
     int corner[3];
     nk_bin_corner(sub_bin[s], g, corner);
     const int h = g.halo;
@@ -223,6 +227,8 @@ k_spread_sm2(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     C *sck2 = reinterpret_cast<C *>(smem_raw + stage_off + 128 + ((32 * W * sizeof(T) + 15) / 16) * 16);
     const int lane = threadIdx.x;
     const int s = blockIdx.x;
+    c += blockIdx.y * g.M;          // batched execute: vector blockIdx.y
+    fine += blockIdx.y * g.ntot;
     int corner[3];
     nk_bin_corner(sub_bin[s], g, corner);
     const int h = g.halo;
@@ -329,7 +335,7 @@ int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
         NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         int64_t stage_off = (p->max_pad_cells * (int64_t)sizeof(C) + 15) / 16 * 16;
-        kern<<<(unsigned)p->S, NW * 32, smem, p->stream>>>(
+        kern<<<dim3((unsigned)p->S, p->ntrans), NW * 32, smem, p->stream>>>(
             p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm, (const T *)p->d_pts,
             p->cap_M, (const C *)c, p->geom, (C *)fine, stage_off, nk_sm3_batch(p->prec));
     } else if (p->method == NK_SM && D == 2) {
@@ -339,12 +345,12 @@ int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
         NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         int64_t stage_off = (p->max_pad_cells * (int64_t)sizeof(C) + 15) / 16 * 16;
-        kern<<<(unsigned)p->S, 32, smem, p->stream>>>(
+        kern<<<dim3((unsigned)p->S, p->ntrans), 32, smem, p->stream>>>(
             p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm, (const T *)p->d_pts,
             p->cap_M, (const C *)c, p->geom, (C *)fine, stage_off);
     } else {
         const int32_t *perm = p->method == NK_GM ? nullptr : p->d_vperm;
-        k_spread_gm<T, D, W><<<(M + 255) / 256, 256, 0, p->stream>>>(
+        k_spread_gm<T, D, W><<<dim3((M + 255) / 256, p->ntrans), 256, 0, p->stream>>>(
             M, perm, p->d_keys, (const T *)p->d_pts, p->cap_M, (const C *)c, p->geom, (C *)fine);
     }
     NK_LAUNCH_CHECK();
@@ -368,7 +374,7 @@ int launch_d(nk_plan *p, const void *c, void *fine, int *launches) {
 }  // namespace
 
 int nk_launch_spread(nk_plan *p, const void *c, void *fine, int *launches) {
-    NK_CUDA(cudaMemsetAsync(fine, 0, p->n_tot * p->csize, p->stream));
+    NK_CUDA(cudaMemsetAsync(fine, 0, p->n_tot * p->csize * p->ntrans, p->stream));
     if (p->prec == NK_DOUBLE)
         return p->dim == 2 ? launch_d<double, 2>(p, c, fine, launches)
                            : launch_d<double, 3>(p, c, fine, launches);

@@ -3,7 +3,9 @@
 Not in the reference (north_star requires them): each is make_plan +
 set_points + execute + destroy.  Precision follows the
 strength / mode dtype (complex64 -> single, else double).  Coordinates are
-1-D arrays x, y[, z] (paper set_pts form).
+1-D arrays x, y[, z] (paper set_pts form).  A leading
+batch axis on the strengths (type 1: (K, M)) or modes (type 2: (K, N_d, ...,
+N_1)) runs K transforms on one set of points (plan n_trans = K).
 """
 
 from __future__ import annotations
@@ -26,6 +28,10 @@ def _type1(coords, c, n_modes, eps, method, out, kwargs):
     n_modes = tuple(int(n) for n in n_modes)
     if len(n_modes) != len(coords):
         raise ValueError(f"n_modes must have {len(coords)} entries")
+    shape = tuple(c.shape)
+    if len(shape) not in (1, 2):
+        raise ValueError(f"strengths must be (M,) or (K, M), got shape {shape}")
+    kwargs.setdefault("n_trans", shape[0] if len(shape) == 2 else 1)
     with TransformPlan(1, n_modes, eps, method, _precision(c), **kwargs) as p:
         p.set_points(*coords)
         return p.execute(c, out)
@@ -34,7 +40,10 @@ def _type1(coords, c, n_modes, eps, method, out, kwargs):
 def _type2(coords, f, eps, method, out, kwargs):
     d = len(coords)
     shape = tuple(f.shape)
-    if len(shape) != d:
+    if len(shape) == d + 1:
+        kwargs.setdefault("n_trans", shape[0])
+        shape = shape[1:]
+    elif len(shape) != d:
         raise ValueError(f"mode array must be {d}-D (N_d, ..., N_1), got shape {shape}")
     with TransformPlan(2, shape[::-1], eps, method, _precision(f), **kwargs) as p:
         p.set_points(*coords)

@@ -97,11 +97,15 @@ class TransformPlan:
         fine: explicit fine-grid sizes (default: the SPEC sizing rule).
         device: CUDA device (default: current).
         timing: record per-stage CUDA events (see stage_times()).
+        n_trans: vectors per execute (cufinufft ``n_trans``; an extension --
+            the reference has no batching).  Inputs and
+            outputs then carry a leading axis of length n_trans; the sort and
+            subproblems of one set_points serve every vector.
     """
 
     def __init__(self, nufft_type, modes, epsilon, method="default", precision="double",
                  workers=0, *, bin_dims=None, max_subproblem=None, fine=None, device=None,
-                 timing=False):
+                 timing=False, n_trans=1):
         if int(workers) < 0:
             raise ValueError(f"worker count must be >= 0, got {workers}")
         if precision not in _COMPLEX:
@@ -121,6 +125,9 @@ class TransformPlan:
         opts.method = _lib.METHODS[method]
         opts.device = self.device
         opts.timing = 1 if timing else 0
+        if int(n_trans) < 1:
+            raise ValueError(f"n_trans must be >= 1, got {n_trans}")
+        opts.n_trans = int(n_trans)
         if bin_dims is not None:
             bin_dims = tuple(int(m) for m in bin_dims)
             if len(bin_dims) != d or any(m < 1 for m in bin_dims):
@@ -156,6 +163,7 @@ class TransformPlan:
                                    precision=precision)
         self.bin_dims = tuple(int(info.bin_dims[i]) for i in range(d))
         self.max_subproblem = int(info.max_subproblem)
+        self.n_trans = int(info.n_trans)
         self.num_points = None
         self._points_kind = None
 
@@ -236,11 +244,17 @@ class TransformPlan:
 
     setpts = set_points   # cufinufft spelling
 
+    def _batch(self, shape):
+        return shape if self.n_trans == 1 else (self.n_trans,) + tuple(shape)
+
     def _io_sizes(self):
+        K = self.n_trans
         Ntot = int(np.prod(self.grid.modes))
         if self.type == 1:
-            return self.num_points, Ntot, (self.num_points,), self.grid.mode_shape
-        return Ntot, self.num_points, self.grid.mode_shape, (self.num_points,)
+            return (K * self.num_points, K * Ntot, self._batch((self.num_points,)),
+                    self._batch(self.grid.mode_shape))
+        return (K * Ntot, K * self.num_points, self._batch(self.grid.mode_shape),
+                self._batch((self.num_points,)))
 
     def execute(self, inp, out=None):
         """type 1 maps M strengths to prod(N) modes shaped
@@ -322,37 +336,38 @@ class TransformPlan:
         return t
 
     def new_fine_grid(self):
-        return torch.empty(self.grid.fine_shape, dtype=_arrays.torch_dtype(_COMPLEX[self.precision]),
+        return torch.empty(self._batch(self.grid.fine_shape),
+                           dtype=_arrays.torch_dtype(_COMPLEX[self.precision]),
                            device=torch.device("cuda", self.device))
 
     def spread_to(self, strengths, fine):
         """Step 1 of type 1: fine <- spread(strengths) (zeroed first)."""
         self._check_points()
-        self._dev(strengths, (self.num_points,), "strengths")
-        self._dev(fine, self.grid.fine_shape, "fine grid")
+        self._dev(strengths, self._batch((self.num_points,)), "strengths")
+        self._dev(fine, self._batch(self.grid.fine_shape), "fine grid")
         self._sync_stream("cuda")
         _lib.check(self._lib.nk_spread(self._h, strengths.data_ptr(), fine.data_ptr()))
         return fine
 
     def fft_(self, fine, direction):
         """cuFFT in place: direction -1 forward, +1 inverse (unnormalised)."""
-        self._dev(fine, self.grid.fine_shape, "fine grid")
+        self._dev(fine, self._batch(self.grid.fine_shape), "fine grid")
         self._sync_stream("cuda")
         _lib.check(self._lib.nk_fft(self._h, fine.data_ptr(), int(direction)))
         return fine
 
     def deconvolve_to(self, fine_spectrum, modes):
         """Step 3 of type 1: modes <- p_k (-1)^{sum k} bhat[k mod n]."""
-        self._dev(fine_spectrum, self.grid.fine_shape, "fine spectrum")
-        self._dev(modes, self.grid.mode_shape, "modes")
+        self._dev(fine_spectrum, self._batch(self.grid.fine_shape), "fine spectrum")
+        self._dev(modes, self._batch(self.grid.mode_shape), "modes")
         self._sync_stream("cuda")
         _lib.check(self._lib.nk_deconv_type1(self._h, fine_spectrum.data_ptr(), modes.data_ptr()))
         return modes
 
     def pad_to(self, modes, fine):
         """Step 1 of type 2: fine <- zero-padded p_k (-1)^{sum k} f_k."""
-        self._dev(modes, self.grid.mode_shape, "modes")
-        self._dev(fine, self.grid.fine_shape, "fine grid")
+        self._dev(modes, self._batch(self.grid.mode_shape), "modes")
+        self._dev(fine, self._batch(self.grid.fine_shape), "fine grid")
         self._sync_stream("cuda")
         _lib.check(self._lib.nk_deconv_type2(self._h, modes.data_ptr(), fine.data_ptr()))
         return fine
@@ -360,8 +375,8 @@ class TransformPlan:
     def interp_to(self, fine, out):
         """Step 3 of type 2: out[j] <- gather at point j."""
         self._check_points()
-        self._dev(fine, self.grid.fine_shape, "fine grid")
-        self._dev(out, (self.num_points,), "output")
+        self._dev(fine, self._batch(self.grid.fine_shape), "fine grid")
+        self._dev(out, self._batch((self.num_points,)), "output")
         self._sync_stream("cuda")
         _lib.check(self._lib.nk_interp(self._h, fine.data_ptr(), out.data_ptr()))
         return out

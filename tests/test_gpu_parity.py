@@ -314,3 +314,44 @@ def test_repeat_execute_and_reuse(nk, orc):
     assert orc.rel_l2_error(a2, a) < 1e-14
     lin = p.execute(2 * c1 - 3j * c2)
     assert orc.rel_l2_error(lin, 2 * a - 3j * b) < 1e-12
+
+
+@pytest.mark.parametrize("dim,nufft_type,prec,method", [
+    (2, 1, "single", "sm"), (2, 2, "single", "sm"), (3, 1, "single", "sm"),
+    (3, 2, "double", "sm"), (2, 1, "double", "gmsort"), (3, 2, "single", "gm")])
+def test_batched_execute_matches_single(nk, dim, nufft_type, prec, method):
+    """n_trans = K (cufinufft ntransf; PAPER.md:220-223 reuse of one setpts):
+    vector k of a batched execute equals a single-vector execute on the same
+    points (same kernels, same order of operations up to float atomics)."""
+    import torch
+    rng = np.random.default_rng(11 + dim + nufft_type)
+    modes = (24, 20) if dim == 2 else (12, 10, 14)
+    M, K, eps = 3000, 3, 1e-6 if prec == "double" else 1e-5
+    cdt = np.complex64 if prec == "single" else np.complex128
+    x = rng.uniform(-np.pi, np.pi, (M, dim))
+    if nufft_type == 1:
+        inp = (rng.standard_normal((K, M)) + 1j * rng.standard_normal((K, M))).astype(cdt)
+    else:
+        shp = (K,) + modes[::-1]
+        inp = (rng.standard_normal(shp) + 1j * rng.standard_normal(shp)).astype(cdt)
+    pb = nk.make_plan(nufft_type, modes, eps, method, prec, n_trans=K)
+    pb.set_points(x)
+    outb = pb.execute(inp)
+    ps = nk.make_plan(nufft_type, modes, eps, method, prec)
+    ps.set_points(x)
+    tol = 1e-12 if prec == "double" else 2e-5
+    for k in range(K):
+        ref = ps.execute(np.ascontiguousarray(inp[k]))
+        assert outb[k].shape == ref.shape
+        assert np.linalg.norm(outb[k] - ref) / np.linalg.norm(ref) < tol
+    # device tensors, batched one-shot
+    xs = [torch.from_numpy(np.ascontiguousarray(x[:, a])).cuda() for a in range(dim)]
+    fn = getattr(nk, f"nufft{dim}d{nufft_type}")
+    if nufft_type == 1:
+        got = fn(*xs, torch.from_numpy(inp).cuda(), modes, eps=eps, method=method)
+    else:
+        got = fn(*xs, torch.from_numpy(inp).cuda(), eps=eps, method=method)
+    assert got.shape == outb.shape
+    assert np.linalg.norm(got.cpu().numpy() - outb) / np.linalg.norm(outb) < tol
+    pb.destroy()
+    ps.destroy()

@@ -517,7 +517,7 @@ static int ensure_point_buffers(nk_plan *p, int64_t M) {
     if (M <= p->cap_M && p->d_keys) return NK_OK;
     void **bufs[] = {(void **)&p->d_keys_in, (void **)&p->d_keys, (void **)&p->d_perm,
                      (void **)&p->d_alt_keys, (void **)&p->d_alt_vals, &p->d_pts,
-                     (void **)&p->d_vperm_buf, &p->d_pts_alt};
+                     (void **)&p->d_vperm_buf, &p->d_pts_alt, (void **)&p->d_sort_scr};
     for (void **b : bufs) {
         if (*b) cudaFree(*b);
         *b = nullptr;
@@ -531,6 +531,8 @@ static int ensure_point_buffers(nk_plan *p, int64_t M) {
     NK_CUDA(cudaMalloc((void **)&p->d_alt_keys, 4 * n));
     NK_CUDA(cudaMalloc((void **)&p->d_alt_vals, 4 * n));
     NK_CUDA(cudaMalloc(&p->d_pts, (size_t)p->csize / 2 * p->dim * n));
+    if (p->method == NK_SM && p->type == 1 && p->dim == 3)
+        NK_CUDA(cudaMalloc((void **)&p->d_sort_scr, 4 * 4 * n));
     if (p->method == NK_SM) {
         NK_CUDA(cudaMalloc((void **)&p->d_vperm_buf, 4 * n));
         NK_CUDA(cudaMalloc(&p->d_pts_alt, (size_t)p->csize / 2 * p->dim * n));
@@ -603,8 +605,7 @@ static int bits_for(int64_t n) {
 static int order_by_start(nk_plan *p) {
     const int64_t M = p->M;
     cudaStream_t st = p->stream;
-    int32_t *scr = nullptr;
-    NK_CUDA(cudaMalloc((void **)&scr, 4 * 4 * (size_t)M));
+    int32_t *scr = p->d_sort_scr;
     int32_t *k0 = scr, *v0 = scr + M, *k1 = scr + 2 * M, *v1 = scr + 3 * M;
     const unsigned nb = blocks_for(M, 256);
     if (p->prec == NK_DOUBLE)
@@ -632,14 +633,7 @@ static int order_by_start(nk_plan *p) {
         std::swap(p->d_pts, p->d_pts_alt);
         p->d_vperm = p->d_vperm_buf;
     }
-    cudaError_t e = cudaStreamSynchronize(st);
-    cudaFree(scr);
-    if (rc) return rc;
-    if (e != cudaSuccess) {
-        nk_set_error(std::string("CUDA error: ") + cudaGetErrorString(e));
-        return NK_ERR_CUDA;
-    }
-    return NK_OK;
+    return rc;
 }
 
 int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, const void *z,

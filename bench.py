@@ -251,7 +251,8 @@ def run_ours(args, cfg):
     setpts_ms = {}
     for t in types:
         method = args.method or "default"
-        plans[t] = nk.make_plan(t, cfg["modes"], cfg["eps"], method, cfg["prec"])
+        kw = {"max_subproblem": args.msub} if args.msub else {}
+        plans[t] = nk.make_plan(t, cfg["modes"], cfg["eps"], method, cfg["prec"], **kw)
         plans[t].set_points(pts_dev)          # first call allocates
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -488,6 +489,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--method", default=None)
+    ap.add_argument("--msub", type=int, default=None, help="max subproblem size override")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-sample", type=int, default=2_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")

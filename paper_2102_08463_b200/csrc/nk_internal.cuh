@@ -94,7 +94,7 @@ struct nk_plan {
     int32_t *d_starts;      // nbins + 1
     void *d_pts;            // dim arrays of cap_M local coords (plan precision)
     int32_t *d_alt_keys, *d_alt_vals;  // radix scratch
-    int32_t *d_sort_scr;    // 4 cap_M int32: (bin, start) ordering scratch (3D type-1 SM)
+    int32_t *d_sort_scr;    // 4 cap_M int32: (bin, start) ordering scratch (type-1 SM)
     int32_t *d_tile_hist;
     int64_t cap_tile_hist;
     int32_t *d_scan_tmp;

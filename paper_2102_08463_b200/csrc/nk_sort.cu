@@ -531,7 +531,7 @@ static int ensure_point_buffers(nk_plan *p, int64_t M) {
     NK_CUDA(cudaMalloc((void **)&p->d_alt_keys, 4 * n));
     NK_CUDA(cudaMalloc((void **)&p->d_alt_vals, 4 * n));
     NK_CUDA(cudaMalloc(&p->d_pts, (size_t)p->csize / 2 * p->dim * n));
-    if (p->method == NK_SM && p->type == 1 && p->dim == 3)
+    if (p->method == NK_SM && p->type == 1)
         NK_CUDA(cudaMalloc((void **)&p->d_sort_scr, 4 * 4 * n));
     if (p->method == NK_SM) {
         NK_CUDA(cudaMalloc((void **)&p->d_vperm_buf, 4 * n));
@@ -714,7 +714,7 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
         }
     }
     p->d_vperm = p->d_perm;
-    if (p->type == 1 && p->method == NK_SM && p->dim == 3 && p->S > 0) {
+    if (p->type == 1 && p->method == NK_SM && p->S > 0) {
         rc = order_by_start(p);
         if (rc) return rc;
     }

@@ -230,6 +230,7 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
 // read-modify-writes (distinct cells per pass, points in sequence): no
 // atomics and no inter-warp conflicts.  Each lane first evaluates one
 // point's kernel rows into shared memory (c folded into the axis-2 row).
+// Runs of points with the same footprint start accumulate in registers.
 template <typename T, int W>
 __global__ void __launch_bounds__(32)
 k_spread_sm2(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
@@ -268,6 +269,24 @@ k_spread_sm2(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
         zero.y = 0;
         buf[i] = zero;
     }
+    C acc[NIT];
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) acc[it].x = acc[it].y = 0;
+    int run = -1;
+    auto flush = [&]() {
+        if (run < 0) return;
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+            if (it < NIT - 1 || last_ok) {
+                C *cell = buf + run + lofs[it];
+                C v = *cell;
+                v.x += acc[it].x;
+                v.y += acc[it].y;
+                *cell = v;
+            }
+            acc[it].x = acc[it].y = 0;
+        }
+    };
     const int j0 = sub_start[s], j1 = sub_stop[s];
     for (int base = j0; base < j1; base += 32) {
         const int nb = min(32, j1 - base);
@@ -290,44 +309,23 @@ k_spread_sm2(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
             sbase[lane] = t2 * p1 + t1;
         }
         __syncwarp();
-        // software-pipelined: point q+1's staged values load during q's RMW
-        int org = sbase[0];
-        C ck[NIT];
-        T k1[NIT];
-#pragma unroll
-        for (int it = 0; it < NIT; ++it) {
-            ck[it] = sck2[lb[it]];
-            k1[it] = sk1[la[it]];
-        }
+        // points arrive in (bin, footprint start) order (setpts K4d): while
+        // the start stays the same the lane's cells accumulate in registers;
+        // a start change writes them back (read-modify-write, no atomics:
+        // the warp owns the padded bin)
         for (int q = 0; q < nb; ++q) {
-            const int qn = min(q + 1, nb - 1);
-            const int orgn = sbase[qn];
-            C ckn[NIT];
-            T k1n[NIT];
-#pragma unroll
-            for (int it = 0; it < NIT; ++it) {
-                ckn[it] = sck2[qn * W + lb[it]];
-                k1n[it] = sk1[qn * W + la[it]];
+            const int org = sbase[q];
+            if (org != run) {   // warp-uniform
+                flush();
+                run = org;
             }
 #pragma unroll
-            for (int it = 0; it < NIT; ++it) {
-                if (it < NIT - 1 || last_ok) {
-                    C *cell = buf + org + lofs[it];
-                    C v = *cell;
-                    v.x += ck[it].x * k1[it];
-                    v.y += ck[it].y * k1[it];
-                    *cell = v;
-                }
-            }
-            __syncwarp();
-            org = orgn;
-#pragma unroll
-            for (int it = 0; it < NIT; ++it) {
-                ck[it] = ckn[it];
-                k1[it] = k1n[it];
-            }
+            for (int it = 0; it < NIT; ++it)
+                acc[it] = nk_fma2(sck2[q * W + lb[it]], sk1[q * W + la[it]], acc[it]);
         }
+        __syncwarp();
     }
+    flush();
     __syncwarp();
     const int o1 = corner[0] - h, o2 = corner[1] - h;
     for (int i = lane; i < P; i += 32) {

@@ -379,74 +379,13 @@ k_refine_interleave(const int32_t *__restrict__ sub_bin, const int32_t *__restri
     }
 }
 
-// ---------------------------------------------------------------- K4c
-// Visit-order refinement by footprint start: inside each subproblem, points
-// are ordered by the padded-bin offset of their footprint origin (axis 1
-// fastest), ties by bin-stable order (deterministic bitonic sort of
-// key << 13 | index in shared memory, <= 8192 points).  Neighbouring lanes
-// then read the same or adjacent padded-bin words, so an 8-byte gather is
-// served by one shared-memory wavefront instead of two or more, and points
-// sharing a start are adjacent (register accumulation in the spread).
-// Only the visit order changes; the exported bin-stable layout is untouched.
-constexpr int START_SORT_MAX = 8192;
-
-template <typename T>
-__global__ void __launch_bounds__(256)
-k_start_sort(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
-             const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm_in,
-             const T *__restrict__ pts_in, int64_t pitch, Geom g,
-             int32_t *__restrict__ perm_out, T *__restrict__ pts_out) {
-    extern __shared__ unsigned skeys[];
-    const int s = blockIdx.x;
-    int corner[3];
-    nk_bin_corner(sub_bin[s], g, corner);
-    const int h = g.halo;
-    const int p1 = min(g.m[0], g.n[0] - corner[0]) + 2 * h;
-    const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
-    const int j0 = sub_start[s], j1 = sub_stop[s];
-    const int n = j1 - j0;
-    int npad = 1;
-    while (npad < n) npad <<= 1;
-    const T half = (T)(0.5 * g.w);
-    for (int i = threadIdx.x; i < npad; i += blockDim.x) {
-        unsigned v = 0xffffffffu;
-        if (i < n) {
-            const int j = j0 + i;
-            const int t1 = (int)nk_ceil<T>(pts_in[j] - half) + h;
-            const int t2 = (int)nk_ceil<T>(pts_in[pitch + j] - half) + h;
-            const int t3 = g.dim == 3 ? (int)nk_ceil<T>(pts_in[2 * pitch + j] - half) + h : 0;
-            v = ((unsigned)((t3 * p2 + t2) * p1 + t1) << 13) | (unsigned)i;
-        }
-        skeys[i] = v;
-    }
-    __syncthreads();
-    for (int k = 2; k <= npad; k <<= 1) {
-        for (int jj = k >> 1; jj > 0; jj >>= 1) {
-            for (int i = threadIdx.x; i < npad; i += blockDim.x) {
-                const int ixj = i ^ jj;
-                if (ixj > i) {
-                    const unsigned a = skeys[i], b = skeys[ixj];
-                    if ((a > b) == ((i & k) == 0)) {
-                        skeys[i] = b;
-                        skeys[ixj] = a;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int src = j0 + (int)(skeys[i] & 8191u);
-        const int d = j0 + i;
-        perm_out[d] = perm_in[src];
-        for (int a = 0; a < g.dim; ++a) pts_out[a * pitch + d] = pts_in[a * pitch + src];
-    }
-}
-
-// ---------------------------------------------------------------- K4d
-// Type-1 visit order (bin, footprint start): start offset of every point in
-// its bin's padded frame, from the visit-order local coordinates (the same
-// T-precision ceil the spread kernel evaluates).
+// ---------------------------------------------------------------- K4c/K4d
+// Visit order (bin, footprint start): start offset of every point in its
+// bin's padded frame, from the visit-order local coordinates (the same
+// T-precision ceil the spread / interp kernels evaluate).  Type 1: points
+// sharing a footprint are adjacent (register run accumulation).  Type 2
+// (single precision): a warp's 32 gathers of one padded-bin row hit adjacent
+// words (one shared-memory wavefront).
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_start_keys(int M, const int32_t *__restrict__ bin_keys, const T *__restrict__ pts,
@@ -531,7 +470,7 @@ static int ensure_point_buffers(nk_plan *p, int64_t M) {
     NK_CUDA(cudaMalloc((void **)&p->d_alt_keys, 4 * n));
     NK_CUDA(cudaMalloc((void **)&p->d_alt_vals, 4 * n));
     NK_CUDA(cudaMalloc(&p->d_pts, (size_t)p->csize / 2 * p->dim * n));
-    if (p->method == NK_SM && p->type == 1)
+    if (p->method == NK_SM)
         NK_CUDA(cudaMalloc((void **)&p->d_sort_scr, 4 * 4 * n));
     if (p->method == NK_SM) {
         NK_CUDA(cudaMalloc((void **)&p->d_vperm_buf, 4 * n));
@@ -598,10 +537,8 @@ static int bits_for(int64_t n) {
     return b;
 }
 
-// Type-1 SM visit order: stable by (bin, footprint start), so points that
-// share a footprint are adjacent across the whole bin and the spread can
-// accumulate them in registers (nk_spread.cu).  Two stable LSD sorts: by
-// start, then by bin key.  The exported bin-stable layout (d_perm) stays.
+// SM visit order: stable by (bin, footprint start).  Two stable LSD sorts:
+// by start, then by bin key.  The exported bin-stable layout (d_perm) stays.
 static int order_by_start(nk_plan *p) {
     const int64_t M = p->M;
     cudaStream_t st = p->stream;
@@ -714,52 +651,24 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
         }
     }
     p->d_vperm = p->d_perm;
-    if (p->type == 1 && p->method == NK_SM && p->S > 0) {
-        rc = order_by_start(p);
-        if (rc) return rc;
-    }
-    if (p->type == 2 && p->method == NK_SM && p->S > 0) {
-        // single precision: footprint-start order (one wavefront per warp
-        // gather row); double: bank-residue interleave (16-byte cells, 3D
-        // w = 13 footprints span many rows), measured faster for each
-        if (p->prec == NK_SINGLE && p->msub <= START_SORT_MAX) {
-            int npad = 1;
-            while (npad < p->msub) npad <<= 1;
-            const size_t smem = 4 * (size_t)npad;
-            if (p->prec == NK_DOUBLE) {
-                NK_CUDA(cudaFuncSetAttribute(k_start_sort<double>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem));
-                k_start_sort<double><<<(unsigned)p->S, 256, smem, st>>>(
-                    p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_perm,
-                    (const double *)p->d_pts, p->cap_M, p->geom, p->d_vperm_buf,
-                    (double *)p->d_pts_alt);
-            } else {
-                NK_CUDA(cudaFuncSetAttribute(k_start_sort<float>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem));
-                k_start_sort<float><<<(unsigned)p->S, 256, smem, st>>>(
-                    p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_perm,
-                    (const float *)p->d_pts, p->cap_M, p->geom, p->d_vperm_buf,
-                    (float *)p->d_pts_alt);
-            }
+    // visit-order refinement inside bins (the exported bin-stable layout is
+    // untouched): (bin, footprint start) for type 1 and single-precision
+    // type 2; bank-residue interleave (K4b) for double-precision type 2
+    // (16-byte cells, w = 13 footprints span many rows: measured faster)
+    if (p->method == NK_SM && p->S > 0) {
+        if (p->type == 1 || p->prec == NK_SINGLE) {
+            rc = order_by_start(p);
+            if (rc) return rc;
         } else {
-            const int G = p->prec == NK_DOUBLE ? 8 : 16;
+            const int G = 8;
             size_t smem = 4 * ((size_t)p->msub + 1);
-            if (p->prec == NK_DOUBLE)
-                k_refine_interleave<double><<<(unsigned)p->S, 256, smem, st>>>(
-                    p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_perm,
-                    (const double *)p->d_pts, p->cap_M, p->geom, G, p->d_alt_keys,
-                    p->d_vperm_buf, (double *)p->d_pts_alt);
-            else
-                k_refine_interleave<float><<<(unsigned)p->S, 256, smem, st>>>(
-                    p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_perm,
-                    (const float *)p->d_pts, p->cap_M, p->geom, G, p->d_alt_keys,
-                    p->d_vperm_buf, (float *)p->d_pts_alt);
+            k_refine_interleave<double><<<(unsigned)p->S, 256, smem, st>>>(
+                p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_perm, (const double *)p->d_pts,
+                p->cap_M, p->geom, G, p->d_alt_keys, p->d_vperm_buf, (double *)p->d_pts_alt);
+            NK_LAUNCH_CHECK();
+            std::swap(p->d_pts, p->d_pts_alt);
+            p->d_vperm = p->d_vperm_buf;
         }
-        NK_LAUNCH_CHECK();
-        std::swap(p->d_pts, p->d_pts_alt);
-        p->d_vperm = p->d_vperm_buf;
     }
     NK_CUDA(cudaStreamSynchronize(st));
     return NK_OK;

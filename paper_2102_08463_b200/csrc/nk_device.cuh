@@ -12,7 +12,17 @@
 // Explicit _rn intrinsics keep nvcc from contracting into FMAs.
 __device__ __forceinline__ double nk_fold(double x, double scale) {
     double a = __dadd_rn(x, NK_PI);
-    double r = fmod(a, NK_TWO_PI);
+    double r;
+    // fast paths, bit-identical to fmod: fmod(a, 2 pi) == a for 0 <= a < 2 pi;
+    // for 2 pi <= a < 4 pi it is a - 2 pi, exact by Sterbenz's lemma; for
+    // -2 pi <= a < 0 it is a and numpy adds 2 pi (rounded, like below)
+    if (a >= 0.0 && a < NK_TWO_PI) {
+        r = a;
+    } else if (a >= NK_TWO_PI && a < 2.0 * NK_TWO_PI) {
+        r = __dsub_rn(a, NK_TWO_PI);
+    } else {
+        r = fmod(a, NK_TWO_PI);
+    }
     if (r != 0.0) {
         if (r < 0.0) r = __dadd_rn(r, NK_TWO_PI);
     } else {

@@ -100,6 +100,50 @@ __device__ __forceinline__ int nk_kernel_row(T u, const Geom &g, T *ker) {
     return (int)st;
 }
 
+// Packed FMA with a broadcast constant addend: (a.x, a.y) * (b.x, b.y) + (c, c)
+// (sm_100 FFMA2 with a 32-bit immediate when c is a compile-time constant).
+__device__ __forceinline__ float2 nk_fma2_cc(float2 a, float2 b, float c) {
+    unsigned long long r;
+    asm("{\n\t.reg .b64 cc;\n\tmov.b64 cc, {%3, %3};\n\tfma.rn.f32x2 %0, %1, %2, cc;\n\t}"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<unsigned long long *>(&a)),
+          "l"(*reinterpret_cast<unsigned long long *>(&b)), "f"(c));
+    return *reinterpret_cast<float2 *>(&r);
+}
+
+// Kernel rows of two axes at once (the 2D footprint, or axes 1-2 in 3D):
+// single precision evaluates both axes' interior Horner pieces as one
+// packed FFMA2 chain per piece (same coefficients, s = (s1, s2)).
+template <typename T, int W>
+__device__ __forceinline__ void nk_kernel_rows2(T u1, T u2, const Geom &g, T *k1, T *k2,
+                                                int &st1, int &st2) {
+    if constexpr (sizeof(T) == 4 && W >= 3) {
+        const float a1 = ceilf(u1 - 0.5f * W), a2 = ceilf(u2 - 0.5f * W);
+        const float d1 = a1 - u1, d2 = a2 - u2;
+        const float z1 = d1 * (2.0f / W), z2 = d2 * (2.0f / W);
+        constexpr float zl = (float)(2.0 * (W - 1) / W);
+        k1[0] = nk_es(z1, g);
+        k2[0] = nk_es(z2, g);
+        k1[W - 1] = nk_es(z1 + zl, g);
+        k2[W - 1] = nk_es(z2 + zl, g);
+        const float2 s = make_float2(fmaf(2.0f, d1, (float)(W - 1)), fmaf(2.0f, d2, (float)(W - 1)));
+        typedef EsPoly<W> P;
+#pragma unroll
+        for (int r = 1; r < W - 1; ++r) {
+            float2 p = make_float2(P::c(r - 1, P::D), P::c(r - 1, P::D));
+#pragma unroll
+            for (int k = P::D - 1; k >= 0; --k) p = nk_fma2_cc(p, s, P::c(r - 1, k));
+            k1[r] = p.x;
+            k2[r] = p.y;
+        }
+        st1 = (int)a1;
+        st2 = (int)a2;
+    } else {
+        st1 = nk_kernel_row<T, W>(u1, g, k1);
+        st2 = nk_kernel_row<T, W>(u2, g, k2);
+    }
+}
+
 // Packed single-precision FMA (sm_100 FFMA2): (a.x, a.y) * b + (c.x, c.y).
 __device__ __forceinline__ float2 nk_fma2(float2 a, float b, float2 c) {
     unsigned long long r;

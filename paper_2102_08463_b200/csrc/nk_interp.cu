@@ -68,8 +68,10 @@ k_interp_gm(int M, const int32_t *__restrict__ perm, const int32_t *__restrict__
     int corner[3];
     nk_bin_corner(keys[j], g, corner);
     T k1[W], k2[W];
-    const int s1 = corner[0] + nk_kernel_row<T, W>(pts[j], g, k1);
-    const int s2 = corner[1] + nk_kernel_row<T, W>(pts[pitch + j], g, k2);
+    int s1, s2;
+    nk_kernel_rows2<T, W>(pts[j], pts[pitch + j], g, k1, k2, s1, s2);
+    s1 += corner[0];
+    s2 += corner[1];
     T u3 = 0, st3 = 0;
     if (D == 3) {
         u3 = pts[2 * pitch + j];
@@ -170,8 +172,10 @@ k_interp_staged(int S, const int32_t *__restrict__ sub_bin, const int32_t *__res
                 dstn = __ldcs(perm + jn);
             }
             T k1[W], k2[W];
-            const int t1 = nk_kernel_row<T, W>(u1, g, k1) + h;
-            const int t2 = nk_kernel_row<T, W>(u2, g, k2) + h;
+            int t1, t2;
+            nk_kernel_rows2<T, W>(u1, u2, g, k1, k2, t1, t2);
+            t1 += h;
+            t2 += h;
             T st3 = 0;
             if (D == 3) st3 = nk_ceil<T>(u3 - (T)(0.5 * W));
             const int t3 = (int)st3 + (D == 3 ? h : 0);

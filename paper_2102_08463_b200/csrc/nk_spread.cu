@@ -26,8 +26,10 @@ k_spread_gm(int M, const int32_t *__restrict__ perm, const int32_t *__restrict__
     const int src = perm ? perm[j] : j;
     const C cv = c[src];
     T k1[W], k2[W];
-    const int s1 = corner[0] + nk_kernel_row<T, W>(pts[j], g, k1);
-    const int s2 = corner[1] + nk_kernel_row<T, W>(pts[pitch + j], g, k2);
+    int s1, s2;
+    nk_kernel_rows2<T, W>(pts[j], pts[pitch + j], g, k1, k2, s1, s2);
+    s1 += corner[0];
+    s2 += corner[1];
     T u3 = 0, st3 = 0;
     if (D == 3) {
         u3 = pts[2 * pitch + j];
@@ -167,13 +169,16 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
         for (int q = threadIdx.x; q < nb; q += blockDim.x) {
             const int j = base + q;
             const C cv = c[perm[j]];
-            T k[W];
-            const int t1 = nk_kernel_row<T, W>(pts[j], g, k) + h;
+            T k[W], kb[W];
+            int t1, t2;
+            nk_kernel_rows2<T, W>(pts[j], pts[pitch + j], g, k, kb, t1, t2);
+            t1 += h;
+            t2 += h;
 #pragma unroll
-            for (int r = 0; r < W; ++r) sk1[q * W + r] = k[r];
-            const int t2 = nk_kernel_row<T, W>(pts[pitch + j], g, k) + h;
-#pragma unroll
-            for (int r = 0; r < W; ++r) sk2[q * W + r] = k[r];
+            for (int r = 0; r < W; ++r) {
+                sk1[q * W + r] = k[r];
+                sk2[q * W + r] = kb[r];
+            }
             const int t3 = nk_kernel_row<T, W>(pts[2 * pitch + j], g, k) + h;
 #pragma unroll
             for (int r = 0; r < W; ++r) {
@@ -294,11 +299,13 @@ k_spread_sm2(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
         if (lane < nb) {
             const int j = base + lane;
             const C cv = c[perm[j]];
-            T k[W];
-            const int t1 = nk_kernel_row<T, W>(pts[j], g, k) + h;
+            T ka[W], k[W];
+            int t1, t2;
+            nk_kernel_rows2<T, W>(pts[j], pts[pitch + j], g, ka, k, t1, t2);
+            t1 += h;
+            t2 += h;
 #pragma unroll
-            for (int r = 0; r < W; ++r) sk1[lane * W + r] = k[r];
-            const int t2 = nk_kernel_row<T, W>(pts[pitch + j], g, k) + h;
+            for (int r = 0; r < W; ++r) sk1[lane * W + r] = ka[r];
 #pragma unroll
             for (int r = 0; r < W; ++r) {
                 C v;

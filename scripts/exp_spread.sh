@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT
-python -m pytest tests -m gpu -q -x -k "sort or fold or bin or golden or layout or nonfinite or nan" 2>&1 | tail -2
+python -m pytest tests -m gpu -q -x 2>&1 | tail -2
 b() { python bench.py --no-cpu-baseline --config $2 --steps ${3:-5} ${4} 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin); print('$1 $2 $4', '%.3e'%d['value'], d['stage_ms'], d['setpts_ms'])"; }
-for c in c2 c3a; do b new $c; done
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_ --csv python bench.py --no-cpu-baseline --config c2 --steps 1 --warmup 3 2>/dev/null | grep -v "^==" | head -40 > gpurun_out/setpts_launch.csv
+for c in c2 c1 c3a c3t2u c3t1u; do b new $c; done

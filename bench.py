@@ -276,8 +276,6 @@ def run_ours(args, cfg):
             runners[t] = ShardedPlan(CudaStageOps(plans[t]), t, root=0)
         else:
             runners[t] = ReplicaPlan(plans[t])   # world 1, or independent replicas (c5)
-    ev_a = torch.cuda.Event(enable_timing=True)
-    ev_b = torch.cuda.Event(enable_timing=True)
     dom_in_step = []
 
     def step():
@@ -292,6 +290,8 @@ def run_ours(args, cfg):
                 r.execute(f_dev if t == 2 else c_dev, out_t2 if t == 2 else out_t1)
                 launches += plans[t].last_launch_count()
             elif t == 1:
+                ev_a = torch.cuda.Event(enable_timing=True)
+                ev_b = torch.cuda.Event(enable_timing=True)
                 ev_a.record()
                 fine = r.ops.spread(c_dev)
                 ev_b.record()
@@ -304,6 +304,8 @@ def run_ours(args, cfg):
             else:
                 dist.broadcast(f_dev, src=0)
                 fine = r.ops.pad_ifft(f_dev)
+                ev_a = torch.cuda.Event(enable_timing=True)
+                ev_b = torch.cuda.Event(enable_timing=True)
                 ev_a.record()
                 r.ops.interp(fine, out_t2)
                 ev_b.record()
@@ -316,8 +318,6 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    start = torch.cuda.Event(enable_timing=True)
-    end = torch.cuda.Event(enable_timing=True)
     step_ms, dom_ms, launches = [], [], 0
     dom_type = types[0]
     with Clocks(local) as clk:
@@ -329,17 +329,30 @@ def run_ours(args, cfg):
             step()
             torch.cuda.synchronize()
         n_pre = len(clk.lines)
+        # K steps back to back, bracketed by barrier + synchronize; before
+        # each step a 256 MiB write flushes L2 (asynchronous, same stream:
+        # it also covers the host's enqueue of the next step, so the step
+        # events see device time only)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        dom_in_step.clear()
+        evs = []
         for _ in range(args.steps):
             flush.fill_(1.0)                       # L2 flush between timed steps
-            torch.cuda.synchronize()
-            start.record()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
             launches += step()
-            end.record()
-            torch.cuda.synchronize()
-            step_ms.append(start.elapsed_time(end))
-            if sharded:
-                dom_ms.append(dom_in_step[-1][0].elapsed_time(dom_in_step[-1][1]))
-                dom_in_step.clear()
+            b.record()
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        step_ms = [a.elapsed_time(b) for a, b in evs]
+        if sharded:
+            dom_ms = [a.elapsed_time(b) for a, b in dom_in_step]
+            dom_in_step.clear()
         # dominant-kernel time for the roofline: same steps again with the
         # plan's per-stage CUDA events on (direct launches, no graph replay)
         stage = None

@@ -237,10 +237,19 @@ def run_ours(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test knobs for exercising the N > 1 path on a one-GPU box: every rank
+    # on cuda:0 over gloo (type-1 grids then all-reduced: gloo has no CUDA
+    # reduce).  Production runs use NCCL, one GPU per rank.
+    backend = os.environ.get("NK_DIST_BACKEND", "nccl")
+    if os.environ.get("NK_BENCH_SAME_DEVICE"):
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     import paper_2102_08463_b200 as nk
 
@@ -296,7 +305,10 @@ def run_ours(args, cfg):
                 fine = r.ops.spread(c_dev)
                 ev_b.record()
                 dom_in_step.append((ev_a, ev_b))
-                dist.reduce(fine, dst=0)
+                if backend == "nccl":
+                    dist.reduce(fine, dst=0)
+                else:
+                    dist.all_reduce(fine)
                 launches += 1
                 if rank == 0:
                     r.ops.fft_deconvolve(fine, out_t1)
@@ -325,9 +337,20 @@ def run_ours(args, cfg):
         # (untimed) until the sampler has readings on both sides of it
         t_pre = time.time()
         soak = 0.0 if os.environ.get("NK_BENCH_NO_CLOCKS") else 5.0
-        while len(clk.lines) < 3 and time.time() - t_pre < soak:
-            step()
-            torch.cuda.synchronize()
+
+        def soak_while(cond):
+            # rank 0 decides: with a collective inside step() every rank
+            # must run the same number of soak steps
+            while True:
+                go = torch.tensor([1 if cond() else 0], device=dev, dtype=torch.int32)
+                if world > 1:
+                    dist.broadcast(go, src=0)
+                if not int(go.item()):
+                    return
+                step()
+                torch.cuda.synchronize()
+
+        soak_while(lambda: len(clk.lines) < 3 and time.time() - t_pre < soak)
         n_pre = len(clk.lines)
         # K steps back to back, bracketed by barrier + synchronize; before
         # each step a 256 MiB write flushes L2 (asynchronous, same stream:
@@ -368,9 +391,7 @@ def run_ours(args, cfg):
             stage = st
             plans[dom_type].set_timing(False)
         t_post = time.time()
-        while len(clk.lines) < n_pre + 3 and time.time() - t_post < soak:
-            step()
-            torch.cuda.synchronize()
+        soak_while(lambda: len(clk.lines) < n_pre + 3 and time.time() - t_post < soak)
     tot_ms = float(np.sum(step_ms))
     dom_avg = float(np.mean(dom_ms)) if dom_ms else None
     if world > 1:

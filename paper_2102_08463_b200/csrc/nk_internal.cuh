@@ -130,8 +130,9 @@ struct nk_plan {
 
 // Warps per CTA of the plane-owned 3D SM spread (nk_spread.cu): warp w owns
 // padded-bin planes z == w (mod NW), ceil(w / NW) planes per footprint.  4
-// measured fastest for w <= 8 (C3: 1.87 ms vs 2.35 ms with 8, 2.38 with 2).
-constexpr int nk_sm3_warps(int w) { return w <= 8 ? 4 : 16; }
+// measured fastest for w <= 8 (C3: 1.87 ms vs 2.35 ms with 8, 2.38 with 2);
+// above, NW = w: every warp owns exactly one plane of every footprint.
+constexpr int nk_sm3_warps(int w) { return w <= 8 ? 4 : w; }
 // Points staged per batch by the plane-owned 3D SM spread (nk_spread.cu).
 inline int nk_sm3_batch(int prec) { return prec == NK_DOUBLE ? 64 : 128; }
 // Dynamic shared memory (bytes) of the SM spread / staged interp for a plan
@@ -142,7 +143,7 @@ inline int64_t nk_sm_smem_bytes(int type, int dim, int prec, int w, const int *b
     for (int i = 0; i < dim; ++i) cells *= bin_dims[i] + 2 * halo;
     int64_t rs = prec == NK_DOUBLE ? 8 : 4;
     int64_t b = (cells * 2 * rs + 15) / 16 * 16;
-    if (type == 1 && dim == 3) b += (int64_t)nk_sm3_batch(prec) * (4 * w * rs + 8);
+    if (type == 1 && dim == 3) b += (int64_t)nk_sm3_batch(prec) * (4 * w * rs + 16);
     if (type == 1 && dim == 2) b += 128 + (32 * w * rs + 15) / 16 * 16 + 32 * w * 2 * rs;
     return b;
 }

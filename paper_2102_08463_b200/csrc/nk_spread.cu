@@ -67,14 +67,22 @@ k_spread_gm(int M, const int32_t *__restrict__ perm, const int32_t *__restrict__
 // p3 cells, Eq. (16)).  Points are staged in batches: each thread evaluates
 // one point's three kernel rows (c folded into the axis-3 row) into shared
 // memory.  Every warp walks the whole batch; warp w only touches padded-bin
-// planes z == w (mod NW), its lanes covering distinct (a, b) cells of a
-// plane, so plain read-modify-write replaces the CAS loops that
-// atomicAdd(float/double) compiles to on shared memory.  Points arrive in
-// (bin, footprint start) order (setpts K4d); while the start stays the same
-// a lane keeps its cells' sums in registers and writes them to shared memory
-// only when the start changes (clustered points: one read-modify-write per
-// run instead of per point).  The finished bin is merged with native global
-// vector reductions (Eq. (17)).
+// planes z == w (mod NW), its lanes covering distinct cells of a plane, so
+// plain read-modify-write replaces the CAS loops that atomicAdd(float /
+// double) compiles to on shared memory.  Points arrive in (bin, t3, t2, t1)
+// footprint-start order (setpts K4d) and a lane keeps its cells' sums in
+// registers while consecutive points fit the warp's register window:
+//  * single precision: window = the point's w x w footprint (lane idx =
+//    it * 32 + lane); runs of identical starts (clustered points) write
+//    shared memory once per run.
+//  * double precision (w = 13, uniform density): window = 16 x-cells x w
+//    rows anchored at the first point of a group; points with the same
+//    (t2, t3) and t1 within 16 - w of the anchor join the group, each lane
+//    adding k1[x - t1] k2[b] c k3[e] for its (x, b).  One shared
+//    read-modify-write per group instead of per point and footprint cell
+//    (the f64 kernel is shared-bandwidth bound: 13 x 13 x 16 B x 2 per
+//    point and plane otherwise).
+// The finished bin is merged with native global vector reductions (Eq. 17).
 template <typename T, int W, int NW>
 __global__ void __launch_bounds__(NW * 32)
 k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
@@ -82,20 +90,13 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
              const T *__restrict__ pts, int64_t pitch, const typename cplx<T>::t *__restrict__ c,
              Geom g, typename cplx<T>::t *__restrict__ fine, int64_t stage_off, int nbatch) {
     typedef typename cplx<T>::t C;
-    // lane -> footprint cell (a, b) of a plane pass.  Double precision (one
-    // 16-byte cell per lane, 8 lanes per shared-memory wavefront): 8 lanes
-    // along a, 4 along b, passes tile the w x w footprint in 8 x 4 blocks, so
-    // each wavefront reads 8 contiguous cells (bank-conflict free; 8 passes
-    // at w = 13 instead of 6 linear ones with 2-way conflicts).  Single
-    // precision: linear idx = it * 32 + lane (fewer idle lanes).  Measured:
-    // blocks win for f64 (C4 type 1 482 -> 442 ms), linear wins for f32.
-    constexpr bool BLK = sizeof(T) == 8;
-    constexpr int NPA = (W + 7) / 8, NPB = (W + 3) / 4;
-    constexpr int NIT = BLK ? NPA * NPB : (W * W + 31) / 32;
-    constexpr int NE = (W + NW - 1) / NW;   // planes per warp per footprint
+    constexpr bool XWIN = sizeof(T) == 8 && W <= 16;
+    constexpr int XW = 16;                      // x-window width (XWIN)
+    constexpr int NIT = XWIN ? (W + 1) / 2 : (W * W + 31) / 32;
+    constexpr int NE = (W + NW - 1) / NW;       // planes per warp per footprint
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *buf = reinterpret_cast<C *>(smem_raw);
-    int2 *sst = reinterpret_cast<int2 *>(smem_raw + stage_off);
+    int4 *sst = reinterpret_cast<int4 *>(smem_raw + stage_off);   // t1, t2, t3
     T *sk1 = reinterpret_cast<T *>(sst + nbatch);
     T *sk2 = sk1 + nbatch * W;
     C *sck3 = reinterpret_cast<C *>(sk2 + nbatch * W);
@@ -110,21 +111,22 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
     const int p3 = min(g.m[2], g.n[2] - corner[2]) + 2 * h;
     const int P = p1 * p2 * p3, pstride = p1 * p2;
+    // lane -> window cell (a = x, b) of each pass
     int la[NIT], lb[NIT], lofs[NIT];
     bool lok[NIT];
 #pragma unroll
     for (int it = 0; it < NIT; ++it) {
-        if (BLK) {
-            la[it] = (it % NPA) * 8 + (lane & 7);
-            lb[it] = (it / NPA) * 4 + (lane >> 3);
-            lok[it] = la[it] < W && lb[it] < W;
+        if (XWIN) {
+            la[it] = lane & (XW - 1);
+            lb[it] = (lane >> 4) + 2 * it;
+            lok[it] = lb[it] < W;
         } else {
             const int idx = it * 32 + lane;
             lb[it] = idx / W;
             la[it] = idx - lb[it] * W;
             lok[it] = idx < W * W;
         }
-        la[it] = min(la[it], W - 1);
+        la[it] = XWIN ? la[it] : min(la[it], W - 1);
         lb[it] = min(lb[it], W - 1);
         lofs[it] = lb[it] * p1 + la[it];
     }
@@ -139,9 +141,11 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     for (int k = 0; k < NE; ++k)
 #pragma unroll
         for (int it = 0; it < NIT; ++it) acc[k][it].x = acc[k][it].y = 0;
-    int run_off = -1, e0 = 0;
-    // add the register sums of the current run to its planes, then clear
-    // (lanes outside the footprint hold sums of clamped cells: never written)
+    // current window: origin offset in the padded bin, its row offset and
+    // x (XWIN), the warp's first plane
+    int run_off = -1, run_row = -1, run_x0 = 0, e0 = 0;
+    // add the register sums of the window to its planes, then clear
+    // (lanes outside the footprint / window never write)
     auto flush = [&]() {
 #pragma unroll
         for (int k = 0; k < NE; ++k) {
@@ -150,7 +154,9 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
                 C *plane = buf + run_off + e * pstride;
 #pragma unroll
                 for (int it = 0; it < NIT; ++it) {
-                    if ((!BLK && it < NIT - 1) || lok[it]) {
+                    const bool ok = XWIN ? (lok[it] && run_x0 + la[it] < p1)
+                                         : ((it < NIT - 1) || lok[it]);
+                    if (ok) {
                         C *cell = plane + lofs[it];
                         C v = *cell;
                         v.x += acc[k][it].x;
@@ -172,8 +178,6 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
             T k[W], kb[W];
             int t1, t2;
             nk_kernel_rows2<T, W>(pts[j], pts[pitch + j], g, k, kb, t1, t2);
-            t1 += h;
-            t2 += h;
 #pragma unroll
             for (int r = 0; r < W; ++r) {
                 sk1[q * W + r] = k[r];
@@ -187,21 +191,36 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
                 v.y = cv.y * k[r];
                 sck3[q * W + r] = v;
             }
-            sst[q] = make_int2((t3 * p2 + t2) * p1 + t1, t3);
+            sst[q] = make_int4(t1 + h, t2 + h, t3, 0);
         }
         __syncthreads();
         for (int q = 0; q < nb; ++q) {
-            const int2 st = sst[q];
-            if (st.x != run_off) {   // uniform across the CTA
+            const int4 st = sst[q];   // (t1, t2, t3) in the padded frame
+            const int row = (st.z * p2 + st.y) * p1;
+            // uniform across the CTA: does point q fit the current window?
+            const bool fits = XWIN ? (row == run_row && st.x - run_x0 <= XW - W)
+                                   : (row + st.x == run_off);
+            if (!fits) {
                 if (run_off >= 0) flush();
-                run_off = st.x;
-                e0 = (warp - st.y) & (NW - 1);
+                run_row = row;
+                run_x0 = st.x;
+                run_off = row + st.x;
+                e0 = ((warp - st.z) % NW + NW) % NW;
             }
             const T *k1q = sk1 + q * W;
             const T *k2q = sk2 + q * W;
             T kk[NIT];
+            if (XWIN) {
+                const int sh = st.x - run_x0;   // point's x offset in the window
 #pragma unroll
-            for (int it = 0; it < NIT; ++it) kk[it] = k2q[lb[it]] * k1q[la[it]];
+                for (int it = 0; it < NIT; ++it) {
+                    const int kx = la[it] - sh;
+                    kk[it] = (kx >= 0 && kx < W) ? k2q[lb[it]] * k1q[kx] : (T)0;
+                }
+            } else {
+#pragma unroll
+                for (int it = 0; it < NIT; ++it) kk[it] = k2q[lb[it]] * k1q[la[it]];
+            }
 #pragma unroll
             for (int k = 0; k < NE; ++k) {
                 const int e = e0 + k * NW;

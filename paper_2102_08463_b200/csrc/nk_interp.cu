@@ -117,7 +117,7 @@ __device__ __forceinline__ void stage_padded_bin(typename cplx<T>::t *buf,
 // are visited in footprint-start order (K4c), so a warp's 32 gathers from
 // one padded-bin row hit adjacent words (one shared-memory wavefront).
 template <typename T, int D, int W, int NBUF>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(NBUF == 1 ? 512 : 256)
 k_interp_staged(int S, const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
                 const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
                 const T *__restrict__ pts, int64_t pitch,
@@ -233,10 +233,13 @@ int launch_w(nk_plan *p, const void *fine, void *out, int *launches) {
         auto kern = two ? k_interp_staged<T, D, W, 2> : k_interp_staged<T, D, W, 1>;
         NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
+        // single-buffer (large padded bin: one CTA per SM) -> 512 threads
+        // share it for latency hiding
+        const int threads = two ? 256 : 512;
         int per_sm = 0;
-        NK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+        NK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
         const int64_t grid = std::min<int64_t>(p->S, (int64_t)std::max(per_sm, 1) * nsm);
-        kern<<<dim3((unsigned)grid, p->ntrans), 256, smem, p->stream>>>(
+        kern<<<dim3((unsigned)grid, p->ntrans), threads, smem, p->stream>>>(
             (int)p->S, p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm,
             (const T *)p->d_pts, p->cap_M, (const C *)fine, p->geom, (C *)out,
             (int)(one / sizeof(C)));

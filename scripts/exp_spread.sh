@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
 b() { python bench.py --no-cpu-baseline --config $2 --steps ${3:-5} ${4} 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin); print('$1 $2 $4', '%.3e'%d['value'], d['stage_ms'], d['setpts_ms'])"; }
-b new c3a; b new c3t1u; b new c5 3; b new c4t1 2
+b new c5 3; b new c4t2 2; b new c2; b new c3t2

@@ -355,3 +355,48 @@ def test_batched_execute_matches_single(nk, dim, nufft_type, prec, method):
     assert np.linalg.norm(got.cpu().numpy() - outb) / np.linalg.norm(outb) < tol
     pb.destroy()
     ps.destroy()
+
+
+@pytest.mark.parametrize("nufft_type", [1, 2])
+def test_graph_replay_on_fixed_buffers(nk, orc, nufft_type):
+    """execute() on the same device (in, out) pair is captured once into a
+    CUDA graph and replayed: replays must see new input contents, a new
+    output buffer or new points (graph invalidated by set_points)."""
+    import torch
+    dev = torch.device("cuda")
+    modes, eps = (48, 40), 1e-9
+    grid = orc.make_grid(modes, eps, "double")
+    rng = np.random.default_rng(5)
+    pts = orc.gen_points("rand", 5000, grid, 5)
+    p = nk.make_plan(nufft_type, modes, eps, "sm")
+    p.set_points(torch.from_numpy(pts).to(dev))
+    shape_in = (5000,) if nufft_type == 1 else modes[::-1]
+    x = lambda: (rng.standard_normal(shape_in) + 1j * rng.standard_normal(shape_in))
+    a = x()
+    inp = torch.from_numpy(a).to(dev)
+    out = p.execute(inp)
+    ref = out.clone()
+    for _ in range(3):                       # direct, capture, replay
+        p.execute(inp, out)
+        assert torch.allclose(out, ref, rtol=1e-12, atol=1e-12 * ref.abs().max().item())
+    b = x()
+    inp.copy_(torch.from_numpy(b))           # same buffer, new contents
+    p.execute(inp, out)
+    direct = orc.direct_type1(pts, b, modes) if nufft_type == 1 else \
+        orc.direct_type2(pts, b, modes)
+    assert orc.rel_l2_error(out.cpu().numpy(), direct) < 10 * eps
+    out2 = torch.empty_like(out)             # new output buffer
+    p.execute(inp, out2)
+    assert torch.equal(out2, out) or torch.allclose(out2, out, rtol=1e-13, atol=0)
+    pts2 = orc.gen_points("cluster", 5000, grid, 6)
+    p.set_points(torch.from_numpy(pts2).to(dev))   # same M, new points
+    p.execute(inp, out)
+    direct2 = orc.direct_type1(pts2, b, modes) if nufft_type == 1 else \
+        orc.direct_type2(pts2, b, modes)
+    assert orc.rel_l2_error(out.cpu().numpy(), direct2) < 10 * eps
+    p.set_timing(True)
+    p.execute(inp, out)
+    st = p.stage_times()
+    assert st["total"] > 0 and st["fft"] > 0
+    p.set_timing(False)
+    p.destroy()

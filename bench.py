@@ -54,6 +54,12 @@ CONFIGS = {
                   prec="single",
                   desc="C3t1u 3D type-1 f32 N=128^3 M=1e7 uniform eps=1e-5 "
                        "(north_star 3D single type-1 target)"),
+    "c5t1": dict(type=1, modes=(128, 128, 128), M=10_000_000, dist="rand", eps=1e-12,
+                 prec="double", desc="C5t1 3D type-1 f64 N=128^3 M=1e7 uniform eps=1e-12 "
+                                     "(the type-1 half of C5)"),
+    "c5t2": dict(type=2, modes=(128, 128, 128), M=10_000_000, dist="rand", eps=1e-12,
+                 prec="double", desc="C5t2 3D type-2 f64 N=128^3 M=1e7 uniform eps=1e-12 "
+                                     "(the type-2 half of C5)"),
     "c4t1": dict(type=1, modes=(256, 256, 256), M=100_000_000, dist="rand", eps=1e-12,
                  prec="double", desc="C4 3D type-1 f64 N=256^3 M=1e8 uniform eps=1e-12"),
     "c4t2": dict(type=2, modes=(256, 256, 256), M=100_000_000, dist="rand", eps=1e-12,
@@ -261,6 +267,8 @@ def run_ours(args, cfg):
     for t in types:
         method = args.method or "default"
         kw = {"max_subproblem": args.msub} if args.msub else {}
+        if args.bins:
+            kw["bin_dims"] = tuple(int(v) for v in args.bins.split(","))
         plans[t] = nk.make_plan(t, cfg["modes"], cfg["eps"], method, cfg["prec"], **kw)
         plans[t].set_points(pts_dev)          # first call allocates
         torch.cuda.synchronize()
@@ -524,6 +532,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--method", default=None)
     ap.add_argument("--msub", type=int, default=None, help="max subproblem size override")
+    ap.add_argument("--bins", default=None, help="bin dims override, e.g. 16,16")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-sample", type=int, default=2_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")

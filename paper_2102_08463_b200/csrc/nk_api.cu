@@ -196,13 +196,13 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
         return NK_ERR_VALUE;
     }
     // M_sub: the reference default is 1024 (binsort.py:38).  A plan that is
-    // not given one picks the B200-tuned size for its kernel: 256 for the
+    // not given one picks the B200-tuned size for its kernel: 128 for the
     // one-warp 2D spread (more warps in flight), 4096 for the staged
     // interpolation (one padded-bin load per bin).  Stage-level
     // build_subproblems keeps the reference default.
     p->msub = opts.max_subproblem ? opts.max_subproblem
                                   : (type == 2 ? 4096
-                                               : (dim == 2 ? 256 : 1024));
+                                               : (dim == 2 ? 128 : 1024));
     if (p->msub < 1) {
         nk_set_error("max subproblem size must be >= 1, got " + std::to_string(p->msub));
         delete p;
@@ -230,6 +230,27 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     int method = opts.method;
     const bool user_bins = opts.bin_dims[0] || opts.bin_dims[1] || opts.bin_dims[2];
     if (method == NK_METHOD_DEFAULT) method = NK_SM;
+    // B200-tuned bin shapes for the SM kernels when the caller gave none
+    // (measured sweeps): smaller padded bins keep more CTAs
+    // (or the 2D one-warp subproblems) resident per SM.  GM / GM-sort and the
+    // stage-level bin_sort keep the reference defaults (binsort.py:34-35).
+    if (method == NK_SM && !user_bins) {
+        static const int t1_2d[3] = {16, 8, 1}, t1_3s[3] = {4, 8, 4}, t1_3d[3] = {16, 8, 4},
+                         t2_2d[3] = {32, 32, 1}, t2_3s[3] = {16, 16, 4}, t2_3d[3] = {8, 8, 8};
+        const int *tb = type == 1 ? (dim == 2 ? t1_2d : (precision == NK_SINGLE ? t1_3s : t1_3d))
+                                  : (dim == 2 ? t2_2d : (precision == NK_SINGLE ? t2_3s : t2_3d));
+        p->nbins = 1;
+        for (int i = 0; i < 3; ++i) {
+            p->bin_dims[i] = i < dim ? tb[i] : 1;
+            p->nb[i] = (p->n[i] + p->bin_dims[i] - 1) / p->bin_dims[i];
+            p->nbins *= p->nb[i];
+        }
+        if (p->nbins >= (1ll << 30)) {
+            nk_set_error("too many bins");
+            delete p;
+            return NK_ERR_VALUE;
+        }
+    }
     int64_t need = nk_sm_smem_bytes(type, dim, precision, w, p->bin_dims, p->halo);
     if (method == NK_SM && need > smem_optin) {
         if (user_bins) {

@@ -129,10 +129,11 @@ struct nk_plan {
 };
 
 // Warps per CTA of the plane-owned 3D SM spread (nk_spread.cu): warp w owns
-// padded-bin planes z == w (mod NW), ceil(w / NW) planes per footprint.  4
-// measured fastest for w <= 8 (C3: 1.87 ms vs 2.35 ms with 8, 2.38 with 2);
-// above, NW = w: every warp owns exactly one plane of every footprint.
-constexpr int nk_sm3_warps(int w) { return w <= 8 ? 4 : w; }
+// padded-bin planes z == w (mod NW), ceil(w / NW) planes per footprint.
+// With the tuned 4 x 8 x 4 bins, 2 measured fastest for w <= 8 (C3a 1.24 ms
+// vs 1.37 with 4, 2.10 with 8, 1.61 with 1); above, NW = w: every warp owns
+// exactly one plane of every footprint.
+constexpr int nk_sm3_warps(int w) { return w <= 8 ? 2 : w; }
 // Points staged per batch by the plane-owned 3D SM spread (nk_spread.cu).
 inline int nk_sm3_batch(int prec) { return prec == NK_DOUBLE ? 64 : 128; }
 // Dynamic shared memory (bytes) of the SM spread / staged interp for a plan

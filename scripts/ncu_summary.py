@@ -35,7 +35,12 @@ def run(rep):
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
             "smsp__inst_executed.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
-            "smsp__sass_inst_executed_op_shared_ld.sum", "smsp__sass_inst_executed_op_shared_st.sum"]
+            "smsp__sass_inst_executed_op_shared_ld.sum", "smsp__sass_inst_executed_op_shared_st.sum",
+            "smsp__sass_inst_executed_op_shared_atom.sum", "smsp__inst_executed_op_global_red.sum",
+            "lts__t_sectors_srcunit_tex_op_red.sum",
+            "lts__t_sectors_srcunit_tex_op_red.sum.pct_of_peak_sustained_elapsed",
+            "lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed",
+            "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
     for k in want:
         if k in h:
             i = h.index(k)

@@ -400,3 +400,66 @@ def test_graph_replay_on_fixed_buffers(nk, orc, nufft_type):
     assert st["total"] > 0 and st["fft"] > 0
     p.set_timing(False)
     p.destroy()
+
+
+def test_method_equivalence_spec2(nk, orc):
+    """SPEC.md:572 acceptance 2: on 20 random instances (M = 1e4, mixed
+    dims / distributions, double) GM, GM-sort and SM agree pairwise within
+    1e-10 relative, for type 1 and type 2."""
+    rng = np.random.default_rng(2024)
+    for inst in range(20):
+        dim = 2 if inst % 2 == 0 else 3
+        dist = "rand" if inst % 4 < 2 else "cluster"
+        modes = (32, 24) if dim == 2 else (12, 16, 10)
+        eps = [1e-6, 1e-9, 1e-12][inst % 3]
+        grid = orc.make_grid(modes, eps, "double")
+        pts = orc.gen_points(dist, 10_000, grid, 100 + inst)
+        c = orc.gen_strengths(10_000, inst)
+        f = rng.standard_normal(modes[::-1]) + 1j * rng.standard_normal(modes[::-1])
+        for t, inp in ((1, c), (2, f)):
+            outs = []
+            for method in ("gm", "gmsort", "sm"):
+                p = nk.make_plan(t, modes, eps, method, "double")
+                p.set_points(pts)
+                outs.append(p.execute(inp))
+                p.destroy()
+            for a in range(3):
+                for b in range(a + 1, 3):
+                    assert orc.rel_l2_error(outs[a], outs[b]) < 1e-10, (inst, t, a, b)
+
+
+def test_spreading_structure_spec5(nk, st, orc):
+    """SPEC.md:575 acceptance 5: a single point spreads onto exactly w^d
+    nonzero cells; translating the point by h_1 shifts the grid by one cell
+    (1e-13); a point next to the seam wraps periodically like the explicit
+    image sum (the oracle's wrapped spread, 1e-12)."""
+    for dim, modes in ((2, (20, 16)), (3, (10, 12, 8))):
+        eps = 1e-9
+        grid = orc.make_grid(modes, eps, "double")
+        params = nk.select_kernel_params(eps, nk.GridSpec(modes, grid.fine), "double")
+        w = params.w
+        gs = nk.GridSpec(modes, grid.fine)
+        x0 = np.full((1, dim), 0.3)
+        one = np.ones(1, np.complex128)
+        for method in ("gm", "sm"):
+            if method == "gm":
+                b0 = st.spread_gm(x0, one, params, gs)
+            else:
+                lay = st.bin_sort(x0, gs)
+                subs = st.build_subproblems(lay, params)
+                b0 = st.spread_sm(x0, lay, subs, one, params, gs)
+            b0 = np.asarray(b0)
+            assert np.count_nonzero(np.abs(b0) > 0) == w ** dim
+        h1 = 2 * np.pi / grid.fine[0]
+        x1 = x0.copy()
+        x1[0, 0] += h1
+        b0 = np.asarray(st.spread_gm(x0, one, params, gs))
+        b1 = np.asarray(st.spread_gm(x1, one, params, gs))
+        assert np.abs(np.roll(b0, 1, axis=-1) - b1).max() <= 1e-13 * np.abs(b0).max()
+        # seam: the point sits half a cell from -pi; its footprint wraps
+        xs = np.full((1, dim), -np.pi + 0.5 * h1)
+        got = np.asarray(st.spread_gm(xs, one, params, gs))
+        oparams = orc.select_kernel_params(eps, grid, "double")
+        ref = np.asarray(orc.spread_gm(xs, one, oparams, grid)).reshape(got.shape)
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+        assert np.count_nonzero(np.abs(got) > 0) == w ** dim

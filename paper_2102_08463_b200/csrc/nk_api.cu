@@ -605,6 +605,12 @@ extern "C" int nk_get_layout(const nk_plan *p, int32_t *point_bins, int32_t *cou
         return NK_ERR_STATE;
     }
     cudaStream_t st = p->stream;
+    if (perm && p->M && !p->perm_valid) {
+        // the plan visits points in (bin, start) order; derive the
+        // reference's bin-stable permutation now (a cached parity export)
+        rc = nk_compute_bin_perm(const_cast<nk_plan *>(p));
+        if (rc) return rc;
+    }
     if (point_bins && p->M)
         NK_CUDA(cudaMemcpyAsync(point_bins, p->d_keys_in, 4 * p->M, cudaMemcpyDefault, st));
     if (counts) NK_CUDA(cudaMemcpyAsync(counts, p->d_counts, 4 * p->nbins, cudaMemcpyDefault, st));

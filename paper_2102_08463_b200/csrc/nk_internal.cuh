@@ -101,6 +101,7 @@ struct nk_plan {
     int64_t cap_scan_tmp;
     unsigned long long *d_bad;
     bool sorted;
+    bool perm_valid;        // d_perm holds the bin-stable layout (else derived on demand)
 
     // subproblems
     int64_t S, cap_S;
@@ -157,6 +158,7 @@ int nk_launch_spread(nk_plan *p, const void *c, void *fine, int *launches);
 int nk_launch_interp(nk_plan *p, const void *fine, void *out, int *launches);
 int nk_launch_deconv1(nk_plan *p, const void *spec, void *modes);
 int nk_launch_deconv2(nk_plan *p, const void *modes, void *spec);
+int nk_compute_bin_perm(nk_plan *p);
 int nk_export_subproblems(const nk_plan *p, int32_t *bin_ids, int32_t *starts,
                           int32_t *stops, int32_t *offsets, int32_t *padded);
 

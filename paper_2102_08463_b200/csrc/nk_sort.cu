@@ -31,17 +31,19 @@ constexpr int SCAN_CHUNK = SCAN_BLOCK * SCAN_ITEMS;
 // unsorted (GM) plans count here (warp-aggregated atomics); sorted plans
 // derive counts/starts from the sorted keys (K2b), free of the same-address
 // atomic contention (2.4k increments per bin at C2).
-template <typename TC>
+template <typename TC, typename T>
 __global__ void __launch_bounds__(256)
 k_fold_keys(int M, const TC *__restrict__ x, const TC *__restrict__ y,
             const TC *__restrict__ z, int64_t stride, Geom g, int32_t *__restrict__ keys,
-            int32_t *__restrict__ counts, unsigned long long *__restrict__ bad) {
+            int32_t *__restrict__ counts, unsigned long long *__restrict__ bad,
+            int32_t *__restrict__ ckeys, int sb) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     bool in = i < M;
     unsigned mask = __ballot_sync(0xffffffffu, in);
     if (!in) return;
     const TC *ax[3] = {x, y, z};
     int key = 0, kstride = 1;
+    int t[3] = {0, 0, 0}, pd[3] = {1, 1, 1};
     bool ok = true;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -50,15 +52,28 @@ k_fold_keys(int M, const TC *__restrict__ x, const TC *__restrict__ y,
             if (!isfinite(xv)) ok = false;
             double v = ok ? nk_fold(xv, g.scale[a]) : 0.0;
             int c = nk_cell(v, g.n[a]);
-            key += kstride * (c / g.m[a]);
+            const int b = c / g.m[a];
+            key += kstride * b;
             kstride *= g.nb[a];
+            if (ckeys) {
+                // footprint start in the bin's padded frame, from the same
+                // plan-precision local coordinate the kernels use (K5)
+                const int corner = b * g.m[a];
+                const T u = (T)(v - (double)corner);
+                t[a] = (int)nk_ceil<T>(u - (T)(0.5 * g.w)) + g.halo;
+                pd[a] = min(g.m[a], g.n[a] - corner) + 2 * g.halo;
+            }
         }
     }
     if (!ok) {
         atomicMin(bad, (unsigned long long)i);
         key = 0;
+        t[0] = t[1] = t[2] = 0;
     }
     keys[i] = key;
+    if (ckeys)
+        ckeys[i] = (int32_t)(((unsigned)key << sb) |
+                             (unsigned)((t[2] * pd[1] + t[1]) * pd[0] + t[0]));
     if (counts) {
         unsigned peers = __match_any_sync(mask, key);
         if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&counts[key], __popc(peers));
@@ -70,11 +85,13 @@ k_fold_keys(int M, const TC *__restrict__ x, const TC *__restrict__ y,
 // starts[nbins] = M) from the bin-sorted keys; counts = adjacent
 // differences.  Identical to bincount + exclusive cumsum (binsort.py:149-151).
 __global__ void __launch_bounds__(256)
-k_bin_starts(int M, int nbins, const int32_t *__restrict__ skeys, int32_t *__restrict__ starts) {
+k_bin_starts(int M, int nbins, const int32_t *__restrict__ skeys, int sb,
+             int32_t *__restrict__ starts) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= M) return;
-    const int k = skeys[i];
-    const int kp = i ? skeys[i - 1] : -1;
+    // (composite keys carry the bin in the bits above sb)
+    const int k = (int)((unsigned)skeys[i] >> sb);
+    const int kp = i ? (int)((unsigned)skeys[i - 1] >> sb) : -1;
     for (int b = kp + 1; b <= k; ++b) starts[b] = i;
     if (i == M - 1)
         for (int b = k + 1; b <= nbins; ++b) starts[b] = M;
@@ -506,11 +523,17 @@ static int ensure_point_buffers(nk_plan *p, int64_t M) {
 }
 
 template <typename TC>
-static int fold_keys(nk_plan *p, const void *x, const void *y, const void *z, int64_t stride) {
+static int fold_keys(nk_plan *p, const void *x, const void *y, const void *z, int64_t stride,
+                     int32_t *ckeys, int sb) {
     int M = (int)p->M;
-    k_fold_keys<TC><<<blocks_for(M, 256), 256, 0, p->stream>>>(
-        M, (const TC *)x, (const TC *)y, (const TC *)z, stride, p->geom, p->d_keys_in,
-        p->method == NK_GM ? p->d_counts : nullptr, p->d_bad);
+    if (p->prec == NK_DOUBLE)
+        k_fold_keys<TC, double><<<blocks_for(M, 256), 256, 0, p->stream>>>(
+            M, (const TC *)x, (const TC *)y, (const TC *)z, stride, p->geom, p->d_keys_in,
+            p->method == NK_GM ? p->d_counts : nullptr, p->d_bad, ckeys, sb);
+    else
+        k_fold_keys<TC, float><<<blocks_for(M, 256), 256, 0, p->stream>>>(
+            M, (const TC *)x, (const TC *)y, (const TC *)z, stride, p->geom, p->d_keys_in,
+            p->method == NK_GM ? p->d_counts : nullptr, p->d_bad, ckeys, sb);
     NK_LAUNCH_CHECK();
     return NK_OK;
 }
@@ -606,11 +629,19 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
     const int nbins = (int)p->nbins;
     cudaStream_t st = p->stream;
     const bool sort = p->method != NK_GM && M > 0;
+    // SM plans (except double-precision type 2) visit points in (bin,
+    // footprint start) order: one LSD radix sort of the composite key
+    // bin << sb | start (K1 computes both).  The exported bin-stable perm is
+    // then derived on demand (nk_export_bin_perm).
+    const int sb = bits_for(p->max_pad_cells);
+    const bool composite = sort && p->method == NK_SM && (p->type == 1 || p->prec == NK_SINGLE) &&
+                           sb + bits_for(nbins) <= 32;
+    int32_t *ck = composite ? p->d_sort_scr : nullptr;
     NK_CUDA(cudaMemsetAsync(p->d_counts, 0, sizeof(int32_t) * nbins, st));
     NK_CUDA(cudaMemsetAsync(p->d_bad, 0xff, sizeof(unsigned long long), st));
     if (M > 0) {
-        rc = coord_prec == NK_DOUBLE ? fold_keys<double>(p, x, y, z, stride)
-                                     : fold_keys<float>(p, x, y, z, stride);
+        rc = coord_prec == NK_DOUBLE ? fold_keys<double>(p, x, y, z, stride, ck, sb)
+                                     : fold_keys<float>(p, x, y, z, stride, ck, sb);
         if (rc) return rc;
     }
     unsigned long long bad = ~0ull;
@@ -623,13 +654,22 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
     }
     const int32_t *perm = nullptr;
     p->sorted = false;
+    p->perm_valid = false;
     if (sort) {
-        rc = radix_sort_pairs(p, p->d_keys_in, nullptr, M, bits_for(p->nbins), p->d_keys,
-                              p->d_perm, p->d_alt_keys, p->d_alt_vals);
+        if (composite) {
+            rc = radix_sort_pairs(p, ck, nullptr, M, sb + bits_for(nbins), p->d_keys,
+                                  p->d_vperm_buf, p->d_alt_keys, p->d_alt_vals);
+            perm = p->d_vperm_buf;
+        } else {
+            rc = radix_sort_pairs(p, p->d_keys_in, nullptr, M, bits_for(p->nbins), p->d_keys,
+                                  p->d_perm, p->d_alt_keys, p->d_alt_vals);
+            perm = p->d_perm;
+            p->perm_valid = true;
+        }
         if (rc) return rc;
-        perm = p->d_perm;
         p->sorted = true;
-        k_bin_starts<<<blocks_for(M, 256), 256, 0, st>>>((int)M, nbins, p->d_keys, p->d_starts);
+        k_bin_starts<<<blocks_for(M, 256), 256, 0, st>>>((int)M, nbins, p->d_keys,
+                                                         composite ? sb : 0, p->d_starts);
         k_counts_from_starts<<<blocks_for(nbins, 256), 256, 0, st>>>(nbins, p->d_starts,
                                                                      p->d_counts);
         NK_LAUNCH_CHECK();
@@ -641,7 +681,6 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
     if (!sort && M > 0) {
         NK_CUDA(cudaMemcpyAsync(p->d_keys, p->d_keys_in, 4 * M, cudaMemcpyDeviceToDevice, st));
     }
-    p->d_vperm = p->d_perm;
     if (M > 0) {
         if (p->prec == NK_DOUBLE)
             rc = coord_prec == NK_DOUBLE ? gather<double, double>(p, perm, x, y, z, stride)
@@ -681,12 +720,14 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
             NK_LAUNCH_CHECK();
         }
     }
-    p->d_vperm = p->d_perm;
+    p->d_vperm = composite ? p->d_vperm_buf : p->d_perm;
     // visit-order refinement inside bins (the exported bin-stable layout is
     // untouched): (bin, footprint start) for type 1 and single-precision
-    // type 2; bank-residue interleave (K4b) for double-precision type 2
-    // (16-byte cells, w = 13 footprints span many rows: measured faster)
-    if (p->method == NK_SM && p->S > 0) {
+    // type 2 (composite sort above, or two stable sorts when the composite
+    // key would exceed 32 bits); bank-residue interleave (K4b) for
+    // double-precision type 2 (16-byte cells, w = 13 footprints span many
+    // rows: measured faster)
+    if (p->method == NK_SM && p->S > 0 && !composite) {
         if (p->type == 1 || p->prec == NK_SINGLE) {
             rc = order_by_start(p);
             if (rc) return rc;
@@ -702,6 +743,18 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
         }
     }
     NK_CUDA(cudaStreamSynchronize(st));
+    return NK_OK;
+}
+
+// The reference's bin-stable permutation (binsort.py:153, stable argsort of
+// the bin keys) for plans whose visit order is (bin, start): one radix sort
+// of the input-order bin keys, run only when the layout is exported.
+int nk_compute_bin_perm(nk_plan *p) {
+    if (p->perm_valid || p->M == 0) return NK_OK;
+    int rc = radix_sort_pairs(p, p->d_keys_in, nullptr, p->M, bits_for(p->nbins), p->d_keys,
+                              p->d_perm, p->d_alt_keys, p->d_alt_vals);
+    if (rc) return rc;
+    p->perm_valid = true;
     return NK_OK;
 }
 

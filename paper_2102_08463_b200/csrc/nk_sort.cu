@@ -205,22 +205,34 @@ k_scan_down(const int32_t *in, int64_t n, const int32_t *__restrict__ partials,
 __global__ void __launch_bounds__(SORT_BLOCK)
 k_radix_hist(const int32_t *__restrict__ keys, int M, int shift, int ntiles,
              int32_t *__restrict__ hist) {
-    __shared__ int h[RADIX];
-    for (int i = threadIdx.x; i < RADIX; i += blockDim.x) h[i] = 0;
+    // per-warp digit histograms with native shared integer atomics (no
+    // match.any: ranks are not needed here), 16-byte key loads
+    __shared__ int h[SORT_WARPS][RADIX];
+    for (int i = threadIdx.x; i < SORT_WARPS * RADIX; i += blockDim.x) (&h[0][0])[i] = 0;
     __syncthreads();
-    int base = blockIdx.x * SORT_TILE;
-    int lane = threadIdx.x & 31;
-#pragma unroll 4
-    for (int it = 0; it < SORT_ITEMS; ++it) {
-        int idx = base + it * SORT_BLOCK + threadIdx.x;
-        bool valid = idx < M;
-        int d = valid ? (keys[idx] >> shift) & (RADIX - 1) : RADIX;
-        unsigned peers = __match_any_sync(0xffffffffu, d);
-        if (valid && lane == __ffs(peers) - 1) atomicAdd(&h[d], __popc(peers));
+    const int warp = threadIdx.x >> 5;
+    const int base = blockIdx.x * SORT_TILE + threadIdx.x * SORT_ITEMS;
+    if (base + SORT_ITEMS <= M) {
+        const int4 *k4 = reinterpret_cast<const int4 *>(keys + base);
+#pragma unroll
+        for (int v = 0; v < SORT_ITEMS / 4; ++v) {
+            const int4 q = __ldg(k4 + v);
+            atomicAdd(&h[warp][(q.x >> shift) & (RADIX - 1)], 1);
+            atomicAdd(&h[warp][(q.y >> shift) & (RADIX - 1)], 1);
+            atomicAdd(&h[warp][(q.z >> shift) & (RADIX - 1)], 1);
+            atomicAdd(&h[warp][(q.w >> shift) & (RADIX - 1)], 1);
+        }
+    } else {
+        for (int it = 0; it < SORT_ITEMS; ++it)
+            if (base + it < M) atomicAdd(&h[warp][(keys[base + it] >> shift) & (RADIX - 1)], 1);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < RADIX; i += blockDim.x)
-        hist[(int64_t)i * ntiles + blockIdx.x] = h[i];
+    for (int i = threadIdx.x; i < RADIX; i += blockDim.x) {
+        int t = 0;
+#pragma unroll
+        for (int w = 0; w < SORT_WARPS; ++w) t += h[w][i];
+        hist[(int64_t)i * ntiles + blockIdx.x] = t;
+    }
 }
 
 __global__ void __launch_bounds__(SORT_BLOCK)

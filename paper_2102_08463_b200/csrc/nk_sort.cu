@@ -15,7 +15,7 @@
 namespace {
 
 constexpr int SORT_BLOCK = 256;
-constexpr int SORT_ITEMS = 16;
+constexpr int SORT_ITEMS = 8;
 constexpr int SORT_TILE = SORT_BLOCK * SORT_ITEMS;  // keys per tile
 constexpr int SORT_WARPS = SORT_BLOCK / 32;
 constexpr int RADIX_BITS = 8;

@@ -463,3 +463,23 @@ def test_spreading_structure_spec5(nk, st, orc):
         ref = np.asarray(orc.spread_gm(xs, one, oparams, grid)).reshape(got.shape)
         assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
         assert np.count_nonzero(np.abs(got) > 0) == w ** dim
+
+
+def test_two_stage_start_order_fallback(nk, orc):
+    """When bin << bits(padded cells) | start would exceed 32 bits (here
+    256^3 unit bins: 24 + 10 bits) setpts falls back to two stable sorts
+    (start, then bin); results must match the GM-sort plan and the exported
+    layout must stay the reference's bin-stable one."""
+    modes, eps, M = (128, 128, 128), 1e-5, 20000
+    grid = orc.make_grid(modes, eps, "single")
+    pts = orc.gen_points("rand", M, grid, 9, np.float32)
+    c = orc.gen_strengths(M, 9).astype(np.complex64)
+    a = nk.make_plan(1, modes, eps, "sm", "single", bin_dims=(1, 1, 1))
+    a.set_points(pts)
+    b = nk.make_plan(1, modes, eps, "gmsort", "single")
+    b.set_points(pts)
+    fa, fb = a.execute(c), b.execute(c)
+    assert orc.rel_l2_error(fa, fb) < 1e-5
+    keys, counts, starts, perm = (t.cpu().numpy() for t in a.layout_tensors())
+    lay = orc.bin_sort(pts, orc.GridSpec(modes, a.grid.fine), (1, 1, 1))
+    assert np.array_equal(perm, lay.perm) and np.array_equal(starts, lay.starts)

@@ -172,26 +172,53 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     for (int base = j0; base < j1; base += nbatch) {
         const int nb = min(nbatch, j1 - base);
         __syncthreads();   // previous batch consumed (and buffer zeroed)
-        for (int q = threadIdx.x; q < nb; q += blockDim.x) {
-            const int j = base + q;
-            const C cv = c[perm[j]];
-            T k[W], kb[W];
-            int t1, t2;
-            nk_kernel_rows2<T, W>(pts[j], pts[pitch + j], g, k, kb, t1, t2);
+        if constexpr (sizeof(T) == 8) {
+            // double: one kernel row (point, axis) per thread -- 3 nb rows
+            // of FP64 exp/sqrt spread over the CTA instead of nb threads
+            int *stt = reinterpret_cast<int *>(sst);
+            for (int v = threadIdx.x; v < 3 * nb; v += blockDim.x) {
+                const int q = v / 3, ax = v - 3 * q;
+                const int j = base + q;
+                T k[W];
+                const int t = nk_kernel_row<T, W>(pts[ax * pitch + j], g, k) + h;
+                if (ax == 2) {
+                    const C cv = c[perm[j]];
 #pragma unroll
-            for (int r = 0; r < W; ++r) {
-                sk1[q * W + r] = k[r];
-                sk2[q * W + r] = kb[r];
-            }
-            const int t3 = nk_kernel_row<T, W>(pts[2 * pitch + j], g, k) + h;
+                    for (int r = 0; r < W; ++r) {
+                        C cvk;
+                        cvk.x = cv.x * k[r];
+                        cvk.y = cv.y * k[r];
+                        sck3[q * W + r] = cvk;
+                    }
+                } else {
+                    T *dstk = (ax == 0 ? sk1 : sk2) + q * W;
 #pragma unroll
-            for (int r = 0; r < W; ++r) {
-                C v;
-                v.x = cv.x * k[r];
-                v.y = cv.y * k[r];
-                sck3[q * W + r] = v;
+                    for (int r = 0; r < W; ++r) dstk[r] = k[r];
+                }
+                stt[q * 4 + ax] = t;
             }
-            sst[q] = make_int4(t1 + h, t2 + h, t3, 0);
+        } else {
+            for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+                const int j = base + q;
+                const C cv = c[perm[j]];
+                T k[W], kb[W];
+                int t1, t2;
+                nk_kernel_rows2<T, W>(pts[j], pts[pitch + j], g, k, kb, t1, t2);
+#pragma unroll
+                for (int r = 0; r < W; ++r) {
+                    sk1[q * W + r] = k[r];
+                    sk2[q * W + r] = kb[r];
+                }
+                const int t3 = nk_kernel_row<T, W>(pts[2 * pitch + j], g, k) + h;
+#pragma unroll
+                for (int r = 0; r < W; ++r) {
+                    C v;
+                    v.x = cv.x * k[r];
+                    v.y = cv.y * k[r];
+                    sck3[q * W + r] = v;
+                }
+                sst[q] = make_int4(t1 + h, t2 + h, t3, 0);
+            }
         }
         __syncthreads();
         for (int q = 0; q < nb; ++q) {

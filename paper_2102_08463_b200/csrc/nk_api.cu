@@ -68,6 +68,8 @@ void free_plan(nk_plan *p) {
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p->fft_ok) cufftDestroy(p->fft);
+    if (p->fft_col_ok) cufftDestroy(p->fft_col);
+    if (p->d_twiddle) cudaFree(p->d_twiddle);
     if (p->gexec) cudaGraphExecDestroy(p->gexec);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     if (p->ev_ok)
@@ -362,6 +364,34 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     }
     p->fft_ok = true;
     cufftSetStream(p->fft, p->stream);
+    // type 2, 2D, single, one vector, n_1 = 2^L in [256, 4096]: pad fused
+    // with the row FFTs; cuFFT only runs the column pass
+    {
+        const int64_t n1 = p->n[0];
+        const char *fe = getenv("NK_FUSED_ROWS");
+        if (type == 2 && dim == 2 && precision == NK_SINGLE && p->ntrans == 1 &&
+            (n1 & (n1 - 1)) == 0 && n1 >= 256 && n1 <= 4096 && !(fe && fe[0] == '0')) {
+            int nc[1] = {(int)p->n[1]};
+            fr = cufftPlanMany(&p->fft_col, 1, nc, nc, (int)n1, 1, nc, (int)n1, 1, CUFFT_C2C,
+                               (int)n1);
+            if (fr == CUFFT_SUCCESS) {
+                p->fft_col_ok = true;
+                cufftSetStream(p->fft_col, p->stream);
+                std::vector<float> twh((size_t)(2 * n1));
+                for (int64_t k = 0; k < n1; ++k) {
+                    const double ang = NK_TWO_PI * (double)k / (double)n1;
+                    twh[2 * k] = (float)cos(ang);
+                    twh[2 * k + 1] = (float)sin(ang);
+                }
+                e = cudaMalloc(&p->d_twiddle, sizeof(float) * 2 * n1);
+                if (e == cudaSuccess)
+                    e = cudaMemcpy(p->d_twiddle, twh.data(), sizeof(float) * 2 * n1,
+                                   cudaMemcpyHostToDevice);
+                p->fused_rows = e == cudaSuccess;
+                if (e != cudaSuccess) cudaGetLastError();
+            }
+        }
+    }
     if (p->timing) {
         for (auto &ev : p->ev) cudaEventCreate(&ev);
         p->ev_ok = true;
@@ -413,6 +443,7 @@ extern "C" int nk_set_stream(nk_plan *p, void *stream) {
     if (rc) return rc;
     p->stream = (cudaStream_t)stream;
     NK_CUFFT(cufftSetStream(p->fft, p->stream));
+    if (p->fft_col_ok) NK_CUFFT(cufftSetStream(p->fft_col, p->stream));
     return NK_OK;
 }
 
@@ -482,12 +513,21 @@ static int execute_device(nk_plan *p, const void *in, void *out) {
         if (rc) return rc;
         launches += p->N_tot > 0;
     } else {
-        rc = nk_launch_deconv2(p, in, p->d_fine);
-        if (rc) return rc;
-        launches += 1;
-        if (p->timing) NK_CUDA(cudaEventRecord(p->ev[1], p->stream));
-        rc = do_fft(p, p->d_fine, +1);
-        if (rc) return rc;
+        if (p->fused_rows) {
+            rc = nk_launch_pad_rowfft(p, in, p->d_fine);
+            if (rc) return rc;
+            launches += 1;
+            if (p->timing) NK_CUDA(cudaEventRecord(p->ev[1], p->stream));
+            NK_CUFFT(cufftExecC2C(p->fft_col, (cufftComplex *)p->d_fine,
+                                  (cufftComplex *)p->d_fine, CUFFT_INVERSE));
+        } else {
+            rc = nk_launch_deconv2(p, in, p->d_fine);
+            if (rc) return rc;
+            launches += 1;
+            if (p->timing) NK_CUDA(cudaEventRecord(p->ev[1], p->stream));
+            rc = do_fft(p, p->d_fine, +1);
+            if (rc) return rc;
+        }
         if (p->timing) NK_CUDA(cudaEventRecord(p->ev[2], p->stream));
         rc = nk_launch_interp(p, p->d_fine, out, &launches);
         if (rc) return rc;
@@ -516,12 +556,14 @@ static int execute_graph(nk_plan *p, const void *in, void *out) {
         cudaStream_t user = p->stream;
         p->stream = p->cap_stream;
         NK_CUFFT(cufftSetStream(p->fft, p->cap_stream));
+        if (p->fft_col_ok) NK_CUFFT(cufftSetStream(p->fft_col, p->cap_stream));
         NK_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
         int rc = execute_device(p, in, out);
         cudaGraph_t graph = nullptr;
         cudaError_t e = cudaStreamEndCapture(p->cap_stream, &graph);
         p->stream = user;
         cufftSetStream(p->fft, user);
+        if (p->fft_col_ok) cufftSetStream(p->fft_col, user);
         if (rc || e != cudaSuccess) {
             if (graph) cudaGraphDestroy(graph);
             cudaGetLastError();

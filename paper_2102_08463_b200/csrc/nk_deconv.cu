@@ -90,6 +90,134 @@ k_deconv2(Geom g, const T *__restrict__ corr, const typename cplx<T>::t *__restr
     }
 }
 
+// K9 + row FFTs fused (type 2, 2D, single precision, n_1 = 2^L <= 4096).
+// One CTA per fine row l_2: rows outside the mode band are written as
+// zeros; band rows load their N_1 corrected modes into shared memory and run
+// an in-place Stockham radix-8 (radix-4 / -2 last stage) inverse FFT (e^{+},
+// unnormalised like cuFFT; twiddle table from FP64 on the host), then write
+// the row once.  The separate pad kernel's full-grid write and the FFT's
+// first full-grid pass disappear; a cuFFT column-only plan finishes the 2D
+// transform.
+__device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// y = DFT_R(v) with kernel e^{+2 pi i k r / R} (inverse direction)
+__device__ __forceinline__ void dft2(float2 &a, float2 &b) {
+    const float2 t = a;
+    a = make_float2(t.x + b.x, t.y + b.y);
+    b = make_float2(t.x - b.x, t.y - b.y);
+}
+__device__ __forceinline__ void dft4(float2 &v0, float2 &v1, float2 &v2, float2 &v3) {
+    const float2 a = make_float2(v0.x + v2.x, v0.y + v2.y), b = make_float2(v0.x - v2.x, v0.y - v2.y);
+    const float2 c = make_float2(v1.x + v3.x, v1.y + v3.y), d = make_float2(v1.x - v3.x, v1.y - v3.y);
+    // i * d = (-d.y, d.x)
+    v0 = make_float2(a.x + c.x, a.y + c.y);
+    v2 = make_float2(a.x - c.x, a.y - c.y);
+    v1 = make_float2(b.x - d.y, b.y + d.x);
+    v3 = make_float2(b.x + d.y, b.y - d.x);
+}
+__device__ __forceinline__ void dft8(float2 *v) {
+    dft4(v[0], v[2], v[4], v[6]);
+    dft4(v[1], v[3], v[5], v[7]);
+    const float c = 0.70710678118654752f;
+    // odd terms times w8^k, w8 = e^{i pi / 4}
+    const float2 o1 = make_float2(c * (v[3].x - v[3].y), c * (v[3].x + v[3].y));
+    const float2 o2 = make_float2(-v[5].y, v[5].x);
+    const float2 o3 = make_float2(-c * (v[7].x + v[7].y), c * (v[7].x - v[7].y));
+    const float2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6], o0 = v[1];
+    v[0] = make_float2(e0.x + o0.x, e0.y + o0.y);
+    v[4] = make_float2(e0.x - o0.x, e0.y - o0.y);
+    v[1] = make_float2(e1.x + o1.x, e1.y + o1.y);
+    v[5] = make_float2(e1.x - o1.x, e1.y - o1.y);
+    v[2] = make_float2(e2.x + o2.x, e2.y + o2.y);
+    v[6] = make_float2(e2.x - o2.x, e2.y - o2.y);
+    v[3] = make_float2(e3.x + o3.x, e3.y + o3.y);
+    v[7] = make_float2(e3.x - o3.x, e3.y - o3.y);
+}
+
+// One Stockham stage of a length-N (power of two) inverse FFT in shared
+// memory (pad cell every 16 entries), radix R = 8 / 4 / 2 chosen at compile
+// time; recursion unrolls the whole transform for a fixed N.
+__device__ __forceinline__ int rpad(int i) { return i + (i >> 4); }
+
+template <int N, int NS>
+__device__ __forceinline__ void rowfft_stages(float2 *xs, const float2 *__restrict__ tw) {
+    if constexpr (NS < N) {
+        constexpr int LEFT = N / NS;
+        constexpr int R = LEFT >= 8 ? 8 : (LEFT >= 4 ? 4 : 2);
+        constexpr int NB = N / R;
+        constexpr int NBT = (NB + 255) / 256;
+        constexpr int TSTEP = N / (NS * R);
+        float2 v[NBT][R];
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < NBT; ++q) {
+            const int j = threadIdx.x + q * 256;
+            if (NB % 256 == 0 || j < NB) {
+                const int k = j & (NS - 1);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    float2 x = xs[rpad(j + r * NB)];
+                    if (r && NS > 1) x = cmulf(x, __ldg(tw + ((k * r * TSTEP) & (N - 1))));
+                    v[q][r] = x;
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < NBT; ++q) {
+            const int j = threadIdx.x + q * 256;
+            if (NB % 256 == 0 || j < NB) {
+                if constexpr (R == 8) dft8(v[q]);
+                else if constexpr (R == 4) dft4(v[q][0], v[q][1], v[q][2], v[q][3]);
+                else dft2(v[q][0], v[q][1]);
+                const int k = j & (NS - 1);
+                const int base = (j - k) * R + k;
+#pragma unroll
+                for (int r = 0; r < R; ++r) xs[rpad(base + r * NS)] = v[q][r];
+            }
+        }
+        rowfft_stages<N, NS * R>(xs, tw);
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(256)
+k_pad_rowfft(Geom g, const float *__restrict__ corr, const float2 *__restrict__ modes,
+             const float2 *__restrict__ tw, float2 *__restrict__ spec) {
+    extern __shared__ __align__(16) float2 xs[];
+    const int n2 = g.n[1];
+    const int N1 = g.N[0], N2 = g.N[1];
+    const int l2 = blockIdx.x;
+    const int i2 = mode_of(l2, N2, n2);
+    float2 *dst = spec + (int64_t)l2 * N;
+    if (i2 < 0) {
+        float4 *d4 = reinterpret_cast<float4 *>(dst);
+#pragma unroll
+        for (int l = threadIdx.x; l < N / 2; l += 256) d4[l] = make_float4(0, 0, 0, 0);
+        return;
+    }
+    const float frow = corr[N1 + i2];
+    const float2 *src = modes + (int64_t)i2 * N1;
+    const int kneg = N1 / 2, kpos = N1 - kneg;
+#pragma unroll
+    for (int l1 = threadIdx.x; l1 < N; l1 += 256) {
+        const int i1 = l1 < kpos ? l1 + kneg : (l1 >= N - kneg ? l1 - N + kneg : -1);
+        float2 v = make_float2(0.f, 0.f);
+        if (i1 >= 0) {
+            v = src[i1];
+            const float f = frow * corr[i1];
+            v.x *= f;
+            v.y *= f;
+        }
+        xs[rpad(l1)] = v;
+    }
+    rowfft_stages<N, 1>(xs, tw);
+    __syncthreads();
+#pragma unroll
+    for (int l = threadIdx.x; l < N; l += 256) dst[l] = xs[rpad(l)];
+}
+
 }  // namespace
 
 int nk_launch_deconv1(nk_plan *p, const void *spec, void *modes) {
@@ -113,6 +241,27 @@ int nk_launch_deconv2(nk_plan *p, const void *modes, void *spec) {
     else
         k_deconv2<float><<<grid, 256, 0, p->stream>>>(p->geom, (const float *)p->d_corr,
                                                       (const float2 *)modes, (float2 *)spec);
+    NK_LAUNCH_CHECK();
+    return NK_OK;
+}
+
+int nk_launch_pad_rowfft(nk_plan *p, const void *modes, void *spec) {
+    const size_t smem = sizeof(float2) * (size_t)(p->n[0] + p->n[0] / 16);
+    const unsigned rows = (unsigned)p->n[1];
+    const float *corr = (const float *)p->d_corr;
+    const float2 *tw = (const float2 *)p->d_twiddle;
+    switch (p->n[0]) {
+#define NK_RF(N)                                                                          \
+    case N:                                                                               \
+        k_pad_rowfft<N><<<rows, 256, smem, p->stream>>>(p->geom, corr, (const float2 *)modes, \
+                                                         tw, (float2 *)spec);             \
+        break;
+        NK_RF(256) NK_RF(512) NK_RF(1024) NK_RF(2048) NK_RF(4096)
+#undef NK_RF
+    default:
+        nk_set_error("fused row FFT: unsupported n_1");
+        return NK_ERR_VALUE;
+    }
     NK_LAUNCH_CHECK();
     return NK_OK;
 }

@@ -483,3 +483,27 @@ def test_two_stage_start_order_fallback(nk, orc):
     keys, counts, starts, perm = (t.cpu().numpy() for t in a.layout_tensors())
     lay = orc.bin_sort(pts, orc.GridSpec(modes, a.grid.fine), (1, 1, 1))
     assert np.array_equal(perm, lay.perm) and np.array_equal(starts, lay.starts)
+
+
+@pytest.mark.parametrize("modes", [(128, 96), (512, 300), (1024, 40)])
+def test_fused_pad_rowfft_type2(nk, orc, modes, monkeypatch):
+    """2D single-precision type 2 with n_1 = 2^L runs K9 fused with the row
+    FFTs (own Stockham radix-8 kernel) + a cuFFT column plan.  Must match
+    direct sums (10 eps) and the unfused pad + 2D cuFFT path."""
+    eps, M = 1e-5, 4000
+    grid = orc.make_grid(modes, eps, "single")
+    assert grid.fine[0] & (grid.fine[0] - 1) == 0
+    pts = orc.gen_points("rand", M, grid, 21, np.float32)
+    rng = np.random.default_rng(3)
+    f = (rng.standard_normal(modes[::-1]) + 1j * rng.standard_normal(modes[::-1]))
+    f = f.astype(np.complex64)
+    p = nk.make_plan(2, modes, eps, "sm", "single")
+    p.set_points(pts)
+    got = p.execute(f)
+    monkeypatch.setenv("NK_FUSED_ROWS", "0")
+    q = nk.make_plan(2, modes, eps, "sm", "single")
+    q.set_points(pts)
+    ref = q.execute(f)
+    assert orc.rel_l2_error(got, ref) < 2e-6
+    if modes[0] * modes[1] * M <= 4e8:
+        assert orc.rel_l2_error(got, orc.direct_type2(pts.astype(np.float64), f, modes)) < 10 * eps

@@ -364,12 +364,13 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     }
     p->fft_ok = true;
     cufftSetStream(p->fft, p->stream);
-    // type 2, 2D, single, one vector, n_1 = 2^L in [256, 4096]: pad fused
-    // with the row FFTs; cuFFT only runs the column pass
+    // 2D, single, one vector, n_1 = 2^L in [256, 4096]: the pad (type 2) or
+    // the deconvolution (type 1) is fused with the row FFTs; cuFFT only runs
+    // the column pass
     {
         const int64_t n1 = p->n[0];
         const char *fe = getenv("NK_FUSED_ROWS");
-        if (type == 2 && dim == 2 && precision == NK_SINGLE && p->ntrans == 1 &&
+        if (dim == 2 && precision == NK_SINGLE && p->ntrans == 1 &&
             (n1 & (n1 - 1)) == 0 && n1 >= 256 && n1 <= 4096 && !(fe && fe[0] == '0')) {
             int nc[1] = {(int)p->n[1]};
             fr = cufftPlanMany(&p->fft_col, 1, nc, nc, (int)n1, 1, nc, (int)n1, 1, CUFFT_C2C,
@@ -506,12 +507,21 @@ static int execute_device(nk_plan *p, const void *in, void *out) {
         rc = nk_launch_spread(p, in, p->d_fine, &launches);
         if (rc) return rc;
         if (p->timing) NK_CUDA(cudaEventRecord(p->ev[1], p->stream));
-        rc = do_fft(p, p->d_fine, -1);
-        if (rc) return rc;
-        if (p->timing) NK_CUDA(cudaEventRecord(p->ev[2], p->stream));
-        rc = nk_launch_deconv1(p, p->d_fine, out);
-        if (rc) return rc;
-        launches += p->N_tot > 0;
+        if (p->fused_rows) {
+            NK_CUFFT(cufftExecC2C(p->fft_col, (cufftComplex *)p->d_fine,
+                                  (cufftComplex *)p->d_fine, CUFFT_FORWARD));
+            if (p->timing) NK_CUDA(cudaEventRecord(p->ev[2], p->stream));
+            rc = nk_launch_rowfft_deconv(p, p->d_fine, out);
+            if (rc) return rc;
+            launches += 1;
+        } else {
+            rc = do_fft(p, p->d_fine, -1);
+            if (rc) return rc;
+            if (p->timing) NK_CUDA(cudaEventRecord(p->ev[2], p->stream));
+            rc = nk_launch_deconv1(p, p->d_fine, out);
+            if (rc) return rc;
+            launches += p->N_tot > 0;
+        }
     } else {
         if (p->fused_rows) {
             rc = nk_launch_pad_rowfft(p, in, p->d_fine);

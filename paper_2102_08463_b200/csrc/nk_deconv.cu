@@ -218,6 +218,36 @@ k_pad_rowfft(Geom g, const float *__restrict__ corr, const float2 *__restrict__ 
     for (int l = threadIdx.x; l < N; l += 256) dst[l] = xs[rpad(l)];
 }
 
+// K8 fused with the row FFTs (type 1, 2D, single precision, n_1 = 2^L):
+// after cuFFT's column pass, CTA i_2 loads fine row (i_2 - N_2/2) mod n_2,
+// runs the forward row FFT in shared memory (forward = conj(inverse(conj))),
+// and writes only the N_1 band modes with the correction factor and phase.
+// The FFT's second full-grid pass and the deconvolution's read disappear.
+template <int N>
+__global__ void __launch_bounds__(256)
+k_rowfft_deconv(Geom g, const float *__restrict__ corr, const float2 *__restrict__ spec,
+                const float2 *__restrict__ tw, float2 *__restrict__ modes) {
+    extern __shared__ __align__(16) float2 xs[];
+    const int N1 = g.N[0], N2 = g.N[1];
+    const int i2 = blockIdx.x;
+    const int l2 = nk_wrap(i2 - N2 / 2, g.n[1]);
+    const float2 *src = spec + (int64_t)l2 * N;
+#pragma unroll
+    for (int l = threadIdx.x; l < N; l += 256) {
+        const float2 v = src[l];
+        xs[rpad(l)] = make_float2(v.x, -v.y);
+    }
+    rowfft_stages<N, 1>(xs, tw);
+    __syncthreads();
+    const float frow = corr[N1 + i2];
+    float2 *dst = modes + (int64_t)i2 * N1;
+    for (int i1 = threadIdx.x; i1 < N1; i1 += 256) {
+        const float2 v = xs[rpad(nk_wrap(i1 - N1 / 2, N))];
+        const float f = frow * corr[i1];
+        dst[i1] = make_float2(v.x * f, -v.y * f);
+    }
+}
+
 }  // namespace
 
 int nk_launch_deconv1(nk_plan *p, const void *spec, void *modes) {
@@ -255,6 +285,28 @@ int nk_launch_pad_rowfft(nk_plan *p, const void *modes, void *spec) {
     case N:                                                                               \
         k_pad_rowfft<N><<<rows, 256, smem, p->stream>>>(p->geom, corr, (const float2 *)modes, \
                                                          tw, (float2 *)spec);             \
+        break;
+        NK_RF(256) NK_RF(512) NK_RF(1024) NK_RF(2048) NK_RF(4096)
+#undef NK_RF
+    default:
+        nk_set_error("fused row FFT: unsupported n_1");
+        return NK_ERR_VALUE;
+    }
+    NK_LAUNCH_CHECK();
+    return NK_OK;
+}
+
+int nk_launch_rowfft_deconv(nk_plan *p, const void *spec, void *modes) {
+    const size_t smem = sizeof(float2) * (size_t)(p->n[0] + p->n[0] / 16);
+    const unsigned rows = (unsigned)p->N[1];
+    const float *corr = (const float *)p->d_corr;
+    const float2 *tw = (const float2 *)p->d_twiddle;
+    switch (p->n[0]) {
+#define NK_RF(N)                                                                          \
+    case N:                                                                               \
+        k_rowfft_deconv<N><<<rows, 256, smem, p->stream>>>(p->geom, corr,                 \
+                                                            (const float2 *)spec, tw,     \
+                                                            (float2 *)modes);             \
         break;
         NK_RF(256) NK_RF(512) NK_RF(1024) NK_RF(2048) NK_RF(4096)
 #undef NK_RF

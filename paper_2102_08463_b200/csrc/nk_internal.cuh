@@ -78,8 +78,8 @@ struct nk_plan {
     void *d_corr;   // per-axis correction factors incl. (2/w) and (-1)^k (plan precision)
     cufftHandle fft;
     bool fft_ok;
-    // type-2 2D single precision with power-of-two n_1: K9 fused with the
-    // row FFTs (nk_deconv.cu, k_pad_rowfft) + a cuFFT column-only plan
+    // 2D single precision with power-of-two n_1: K9 (type 2) / K8 (type 1)
+    // fused with the row FFTs (nk_deconv.cu) + a cuFFT column-only plan
     bool fused_rows;
     cufftHandle fft_col;
     bool fft_col_ok;
@@ -165,6 +165,7 @@ int nk_launch_interp(nk_plan *p, const void *fine, void *out, int *launches);
 int nk_launch_deconv1(nk_plan *p, const void *spec, void *modes);
 int nk_launch_deconv2(nk_plan *p, const void *modes, void *spec);
 int nk_launch_pad_rowfft(nk_plan *p, const void *modes, void *spec);
+int nk_launch_rowfft_deconv(nk_plan *p, const void *spec, void *modes);
 int nk_compute_bin_perm(nk_plan *p);
 int nk_export_subproblems(const nk_plan *p, int32_t *bin_ids, int32_t *starts,
                           int32_t *stops, int32_t *offsets, int32_t *padded);

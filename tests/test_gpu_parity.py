@@ -507,3 +507,23 @@ def test_fused_pad_rowfft_type2(nk, orc, modes, monkeypatch):
     assert orc.rel_l2_error(got, ref) < 2e-6
     if modes[0] * modes[1] * M <= 4e8:
         assert orc.rel_l2_error(got, orc.direct_type2(pts.astype(np.float64), f, modes)) < 10 * eps
+
+
+@pytest.mark.parametrize("modes", [(128, 96), (256, 256), (1024, 40)])
+def test_fused_rowfft_deconv_type1(nk, orc, modes, monkeypatch):
+    """2D single-precision type 1 with n_1 = 2^L: cuFFT column pass, then
+    the forward row FFTs fused with K8 (own kernel).  Must match direct
+    sums (10 eps) and the unfused 2D cuFFT + deconvolution path."""
+    eps, M = 1e-5, 4000
+    grid = orc.make_grid(modes, eps, "single")
+    pts = orc.gen_points("rand", M, grid, 22, np.float32)
+    c = orc.gen_strengths(M, 22).astype(np.complex64)
+    p = nk.make_plan(1, modes, eps, "sm", "single")
+    p.set_points(pts)
+    got = p.execute(c)
+    monkeypatch.setenv("NK_FUSED_ROWS", "0")
+    q = nk.make_plan(1, modes, eps, "sm", "single")
+    q.set_points(pts)
+    ref = q.execute(c)
+    assert orc.rel_l2_error(got, ref) < 2e-6
+    assert orc.rel_l2_error(got, orc.direct_type1(pts.astype(np.float64), c, modes)) < 10 * eps

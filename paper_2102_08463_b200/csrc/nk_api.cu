@@ -364,17 +364,20 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     }
     p->fft_ok = true;
     cufftSetStream(p->fft, p->stream);
-    // 2D, single, one vector, n_1 = 2^L in [256, 4096]: the pad (type 2) or
-    // the deconvolution (type 1) is fused with the row FFTs; cuFFT only runs
-    // the column pass
+    // 2D, single precision, one vector, n_1 = 2^L in [256, 4096]: the pad
+    // (type 2) or the deconvolution (type 1) is fused with the x-row FFTs;
+    // cuFFT only runs the y axis
     {
         const int64_t n1 = p->n[0];
         const char *fe = getenv("NK_FUSED_ROWS");
-        if (dim == 2 && precision == NK_SINGLE && p->ntrans == 1 &&
-            (n1 & (n1 - 1)) == 0 && n1 >= 256 && n1 <= 4096 && !(fe && fe[0] == '0')) {
-            int nc[1] = {(int)p->n[1]};
-            fr = cufftPlanMany(&p->fft_col, 1, nc, nc, (int)n1, 1, nc, (int)n1, 1, CUFFT_C2C,
-                               (int)n1);
+        // 2D only: in 3D the strided rank-2 (z, y) cuFFT plan took 390 us
+        // against 144 us for the whole 3D transform at 256^3
+        if (dim == 2 && precision == NK_SINGLE && p->ntrans == 1 && (n1 & (n1 - 1)) == 0 &&
+            n1 >= 256 && n1 <= 4096 && !(fe && fe[0] == '0')) {
+            // the y axis of every x column: a strided batch of 1D transforms
+            int nc[2] = {(int)p->n[dim - 1], (int)p->n[1]};
+            fr = cufftPlanMany(&p->fft_col, dim - 1, nc, nc, (int)n1, 1, nc, (int)n1, 1,
+                               CUFFT_C2C, (int)n1);
             if (fr == CUFFT_SUCCESS) {
                 p->fft_col_ok = true;
                 cufftSetStream(p->fft_col, p->stream);

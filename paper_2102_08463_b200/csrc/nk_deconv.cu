@@ -90,7 +90,7 @@ k_deconv2(Geom g, const T *__restrict__ corr, const typename cplx<T>::t *__restr
     }
 }
 
-// K9 + row FFTs fused (type 2, 2D, single precision, n_1 = 2^L <= 4096).
+// K9 + row FFTs fused (type 2, 2D/3D, single precision, n_1 = 2^L <= 4096).
 // One CTA per fine row l_2: rows outside the mode band are written as
 // zeros; band rows load their N_1 corrected modes into shared memory and run
 // an in-place Stockham radix-8 (radix-4 / -2 last stage) inverse FFT (e^{+},
@@ -188,17 +188,20 @@ k_pad_rowfft(Geom g, const float *__restrict__ corr, const float2 *__restrict__ 
     extern __shared__ __align__(16) float2 xs[];
     const int n2 = g.n[1];
     const int N1 = g.N[0], N2 = g.N[1];
-    const int l2 = blockIdx.x;
+    const int row = blockIdx.x;            // l2 + n2 * l3
+    const int l2 = row % n2, l3 = row / n2;
     const int i2 = mode_of(l2, N2, n2);
-    float2 *dst = spec + (int64_t)l2 * N;
-    if (i2 < 0) {
+    const int i3 = g.dim == 3 ? mode_of(l3, g.N[2], g.n[2]) : 0;
+    float2 *dst = spec + (int64_t)row * N;
+    if (i2 < 0 || i3 < 0) {
         float4 *d4 = reinterpret_cast<float4 *>(dst);
 #pragma unroll
         for (int l = threadIdx.x; l < N / 2; l += 256) d4[l] = make_float4(0, 0, 0, 0);
         return;
     }
-    const float frow = corr[N1 + i2];
-    const float2 *src = modes + (int64_t)i2 * N1;
+    float frow = corr[N1 + i2];
+    if (g.dim == 3) frow *= corr[N1 + N2 + i3];
+    const float2 *src = modes + ((int64_t)i3 * N2 + i2) * N1;
     const int kneg = N1 / 2, kpos = N1 - kneg;
 #pragma unroll
     for (int l1 = threadIdx.x; l1 < N; l1 += 256) {
@@ -218,7 +221,7 @@ k_pad_rowfft(Geom g, const float *__restrict__ corr, const float2 *__restrict__ 
     for (int l = threadIdx.x; l < N; l += 256) dst[l] = xs[rpad(l)];
 }
 
-// K8 fused with the row FFTs (type 1, 2D, single precision, n_1 = 2^L):
+// K8 fused with the row FFTs (type 1, 2D/3D, single precision, n_1 = 2^L):
 // after cuFFT's column pass, CTA i_2 loads fine row (i_2 - N_2/2) mod n_2,
 // runs the forward row FFT in shared memory (forward = conj(inverse(conj))),
 // and writes only the N_1 band modes with the correction factor and phase.
@@ -229,9 +232,11 @@ k_rowfft_deconv(Geom g, const float *__restrict__ corr, const float2 *__restrict
                 const float2 *__restrict__ tw, float2 *__restrict__ modes) {
     extern __shared__ __align__(16) float2 xs[];
     const int N1 = g.N[0], N2 = g.N[1];
-    const int i2 = blockIdx.x;
+    const int row = blockIdx.x;            // i2 + N2 * i3
+    const int i2 = row % N2, i3 = row / N2;
     const int l2 = nk_wrap(i2 - N2 / 2, g.n[1]);
-    const float2 *src = spec + (int64_t)l2 * N;
+    const int l3 = g.dim == 3 ? nk_wrap(i3 - g.N[2] / 2, g.n[2]) : 0;
+    const float2 *src = spec + ((int64_t)l3 * g.n[1] + l2) * N;
 #pragma unroll
     for (int l = threadIdx.x; l < N; l += 256) {
         const float2 v = src[l];
@@ -239,8 +244,9 @@ k_rowfft_deconv(Geom g, const float *__restrict__ corr, const float2 *__restrict
     }
     rowfft_stages<N, 1>(xs, tw);
     __syncthreads();
-    const float frow = corr[N1 + i2];
-    float2 *dst = modes + (int64_t)i2 * N1;
+    float frow = corr[N1 + i2];
+    if (g.dim == 3) frow *= corr[N1 + N2 + i3];
+    float2 *dst = modes + (int64_t)row * N1;
     for (int i1 = threadIdx.x; i1 < N1; i1 += 256) {
         const float2 v = xs[rpad(nk_wrap(i1 - N1 / 2, N))];
         const float f = frow * corr[i1];
@@ -277,7 +283,7 @@ int nk_launch_deconv2(nk_plan *p, const void *modes, void *spec) {
 
 int nk_launch_pad_rowfft(nk_plan *p, const void *modes, void *spec) {
     const size_t smem = sizeof(float2) * (size_t)(p->n[0] + p->n[0] / 16);
-    const unsigned rows = (unsigned)p->n[1];
+    const unsigned rows = (unsigned)(p->n[1] * p->n[2]);
     const float *corr = (const float *)p->d_corr;
     const float2 *tw = (const float2 *)p->d_twiddle;
     switch (p->n[0]) {
@@ -298,7 +304,7 @@ int nk_launch_pad_rowfft(nk_plan *p, const void *modes, void *spec) {
 
 int nk_launch_rowfft_deconv(nk_plan *p, const void *spec, void *modes) {
     const size_t smem = sizeof(float2) * (size_t)(p->n[0] + p->n[0] / 16);
-    const unsigned rows = (unsigned)p->N[1];
+    const unsigned rows = (unsigned)(p->N[1] * p->N[2]);
     const float *corr = (const float *)p->d_corr;
     const float2 *tw = (const float2 *)p->d_twiddle;
     switch (p->n[0]) {

@@ -505,7 +505,7 @@ def test_fused_pad_rowfft_type2(nk, orc, modes, monkeypatch):
     q.set_points(pts)
     ref = q.execute(f)
     assert orc.rel_l2_error(got, ref) < 2e-6
-    if modes[0] * modes[1] * M <= 4e8:
+    if int(np.prod(modes)) * M <= 4e8:
         assert orc.rel_l2_error(got, orc.direct_type2(pts.astype(np.float64), f, modes)) < 10 * eps
 
 
@@ -526,4 +526,5 @@ def test_fused_rowfft_deconv_type1(nk, orc, modes, monkeypatch):
     q.set_points(pts)
     ref = q.execute(c)
     assert orc.rel_l2_error(got, ref) < 2e-6
-    assert orc.rel_l2_error(got, orc.direct_type1(pts.astype(np.float64), c, modes)) < 10 * eps
+    if int(np.prod(modes)) * M <= 4e8:
+        assert orc.rel_l2_error(got, orc.direct_type1(pts.astype(np.float64), c, modes)) < 10 * eps

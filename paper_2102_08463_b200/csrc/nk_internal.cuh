@@ -137,12 +137,14 @@ struct nk_plan {
 
 // Warps per CTA of the plane-owned 3D SM spread (nk_spread.cu): warp w owns
 // padded-bin planes z == w (mod NW), ceil(w / NW) planes per footprint.
-// With the tuned 4 x 8 x 4 bins, 2 measured fastest for w <= 8 (C3a 1.24 ms
+// With the tuned small bins, 2 measured fastest for w <= 8 (C3a 1.24 ms
 // vs 1.37 with 4, 2.10 with 8, 1.61 with 1); above, NW = w: every warp owns
 // exactly one plane of every footprint.
 constexpr int nk_sm3_warps(int w) { return w <= 8 ? 2 : w; }
-// Points staged per batch by the plane-owned 3D SM spread (nk_spread.cu).
-inline int nk_sm3_batch(int prec) { return prec == NK_DOUBLE ? 64 : 128; }
+// Points staged per batch by the plane-owned 3D SM spread (nk_spread.cu):
+// 64 keeps the staging small enough for more resident CTAs (C3a spread
+// 1.24 -> 1.08 ms vs 128).
+inline int nk_sm3_batch(int prec) { return 64; }
 // Dynamic shared memory (bytes) of the SM spread / staged interp for a plan
 // shape: padded bin (+ point staging for the 3D spread).
 inline int64_t nk_sm_smem_bytes(int type, int dim, int prec, int w, const int *bin_dims,

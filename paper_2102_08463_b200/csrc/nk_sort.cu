@@ -97,6 +97,19 @@ k_bin_starts(int M, int nbins, const int32_t *__restrict__ skeys, int sb,
         for (int b = k + 1; b <= nbins; ++b) starts[b] = M;
 }
 
+// sum_b counts[b]^2 (point-weighted bin density for the visit-order choice)
+__global__ void __launch_bounds__(256)
+k_sum_sq(int nbins, const int32_t *__restrict__ counts, unsigned long long *__restrict__ out) {
+    unsigned long long acc = 0;
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nbins; b += gridDim.x * blockDim.x) {
+        const unsigned long long c = (unsigned)counts[b];
+        acc += c * c;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
 __global__ void __launch_bounds__(256)
 k_counts_from_starts(int nbins, const int32_t *__restrict__ starts, int32_t *__restrict__ counts) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -648,13 +661,12 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
     const int nbins = (int)p->nbins;
     cudaStream_t st = p->stream;
     const bool sort = p->method != NK_GM && M > 0;
-    // SM plans (except double-precision type 2) visit points in (bin,
-    // footprint start) order: one LSD radix sort of the composite key
-    // bin << sb | start (K1 computes both).  The exported bin-stable perm is
-    // then derived on demand (nk_export_bin_perm).
+    // SM plans visit points in (bin, footprint start) order: one LSD radix
+    // sort of the composite key bin << sb | start (K1 computes both).  The
+    // exported bin-stable perm is then derived on demand
+    // (nk_compute_bin_perm).
     const int sb = bits_for(p->max_pad_cells);
-    const bool composite = sort && p->method == NK_SM && (p->type == 1 || p->prec == NK_SINGLE) &&
-                           sb + bits_for(nbins) <= 32;
+    const bool composite = sort && p->method == NK_SM && sb + bits_for(nbins) <= 32;
     int32_t *ck = composite ? p->d_sort_scr : nullptr;
     NK_CUDA(cudaMemsetAsync(p->d_counts, 0, sizeof(int32_t) * nbins, st));
     NK_CUDA(cudaMemsetAsync(p->d_bad, 0xff, sizeof(unsigned long long), st));
@@ -741,24 +753,57 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
     }
     p->d_vperm = composite ? p->d_vperm_buf : p->d_perm;
     // visit-order refinement inside bins (the exported bin-stable layout is
-    // untouched): (bin, footprint start) for type 1 and single-precision
-    // type 2 (composite sort above, or two stable sorts when the composite
-    // key would exceed 32 bits); bank-residue interleave (K4b) for
-    // double-precision type 2 (16-byte cells, w = 13 footprints span many
-    // rows: measured faster)
-    if (p->method == NK_SM && p->S > 0 && !composite) {
-        if (p->type == 1 || p->prec == NK_SINGLE) {
-            rc = order_by_start(p);
+    // untouched).  Start order puts points that share footprint words in the
+    // same warp (broadcast loads, register runs in the spread); at low local
+    // density there is little to share and the staged interpolation is
+    // better served by the bank-residue interleave (K4b: every wavefront
+    // gathers from distinct banks).  Measured (type 2): start wins at C2
+    // (2.4 points per cell: 166 vs 182 us) and for clustered 3D points (0.90
+    // vs 1.35 ms); the interleave wins for uniform 3D f32 at 0.6 points per
+    // cell (0.90 vs 1.17 ms) and f64 (15.3 vs 21.0 ms).  The switch is the
+    // point-weighted bin density sum_b count_b^2 / (M * bin cells).
+    if (p->method == NK_SM && p->S > 0) {
+        if (!composite && p->type == 1) {
+            rc = order_by_start(p);   // composite key would exceed 32 bits
             if (rc) return rc;
-        } else {
-            const int G = 8;
-            size_t smem = 4 * ((size_t)p->msub + 1);
-            k_refine_interleave<double><<<(unsigned)p->S, 256, smem, st>>>(
-                p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_perm, (const double *)p->d_pts,
-                p->cap_M, p->geom, G, p->d_alt_keys, p->d_vperm_buf, (double *)p->d_pts_alt);
-            NK_LAUNCH_CHECK();
-            std::swap(p->d_pts, p->d_pts_alt);
-            p->d_vperm = p->d_vperm_buf;
+        } else if (p->type == 2) {
+            bool interleave = !composite && p->prec == NK_DOUBLE;
+            if (composite) {
+                unsigned long long *d_sq = p->d_bad;   // reused: setpts' error flag is read
+                NK_CUDA(cudaMemsetAsync(d_sq, 0, sizeof(unsigned long long), st));
+                k_sum_sq<<<std::min(blocks_for(nbins, 256), 1184u), 256, 0, st>>>(
+                    nbins, p->d_counts, d_sq);
+                NK_LAUNCH_CHECK();
+                unsigned long long sq = 0;
+                NK_CUDA(cudaMemcpyAsync(&sq, d_sq, sizeof(sq), cudaMemcpyDeviceToHost, st));
+                NK_CUDA(cudaStreamSynchronize(st));
+                double cells = 1;
+                for (int i = 0; i < p->dim; ++i) cells *= p->bin_dims[i];
+                const double rho = (double)sq / ((double)M * cells);
+                interleave = rho < 1.2;
+            } else if (p->prec == NK_SINGLE) {
+                rc = order_by_start(p);   // composite key would exceed 32 bits
+                if (rc) return rc;
+            }
+            if (interleave) {
+                // in: current visit order; out: scratch-backed visit order
+                int32_t *vout = composite ? p->d_sort_scr : p->d_vperm_buf;
+                int32_t *scr = composite ? p->d_sort_scr + p->cap_M : p->d_alt_keys;
+                size_t smem = 4 * ((size_t)p->msub + 1);
+                if (p->prec == NK_DOUBLE)
+                    k_refine_interleave<double><<<(unsigned)p->S, 256, smem, st>>>(
+                        p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm,
+                        (const double *)p->d_pts, p->cap_M, p->geom, 8, scr, vout,
+                        (double *)p->d_pts_alt);
+                else
+                    k_refine_interleave<float><<<(unsigned)p->S, 256, smem, st>>>(
+                        p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm,
+                        (const float *)p->d_pts, p->cap_M, p->geom, 16, scr, vout,
+                        (float *)p->d_pts_alt);
+                NK_LAUNCH_CHECK();
+                std::swap(p->d_pts, p->d_pts_alt);
+                p->d_vperm = vout;
+            }
         }
     }
     NK_CUDA(cudaStreamSynchronize(st));

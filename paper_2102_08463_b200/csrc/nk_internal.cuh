@@ -153,7 +153,11 @@ inline int64_t nk_sm_smem_bytes(int type, int dim, int prec, int w, const int *b
     for (int i = 0; i < dim; ++i) cells *= bin_dims[i] + 2 * halo;
     int64_t rs = prec == NK_DOUBLE ? 8 : 4;
     int64_t b = (cells * 2 * rs + 15) / 16 * 16;
-    if (type == 1 && dim == 3) b += (int64_t)nk_sm3_batch(prec) * (4 * w * rs + 16);
+    // staging per point: int4 start, k1 row (double: zero-padded to 32),
+    // k2 row, c * k3 row (complex)
+    if (type == 1 && dim == 3)
+        b += (int64_t)nk_sm3_batch(prec) *
+             (((prec == NK_DOUBLE && w <= 16) ? 32 : w) * rs + 3 * w * rs + 16);
     if (type == 1 && dim == 2) b += 128 + (32 * w * rs + 15) / 16 * 16 + 32 * w * 2 * rs;
     return b;
 }

@@ -97,8 +97,11 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *buf = reinterpret_cast<C *>(smem_raw);
     int4 *sst = reinterpret_cast<int4 *>(smem_raw + stage_off);   // t1, t2, t3
+    // XWIN: each point's k1 row sits at offset XW of a zero-padded 2 XW row,
+    // so the window gather k1[x - shift] needs no bounds test
+    constexpr int K1P = XWIN ? 2 * XW : W;
     T *sk1 = reinterpret_cast<T *>(sst + nbatch);
-    T *sk2 = sk1 + nbatch * W;
+    T *sk2 = sk1 + nbatch * K1P;
     C *sck3 = reinterpret_cast<C *>(sk2 + nbatch * W);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x;
@@ -191,9 +194,16 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
                         sck3[q * W + r] = cvk;
                     }
                 } else {
-                    T *dstk = (ax == 0 ? sk1 : sk2) + q * W;
+                    if (ax == 0 && XWIN) {
+                        T *dstk = sk1 + q * K1P;
 #pragma unroll
-                    for (int r = 0; r < W; ++r) dstk[r] = k[r];
+                        for (int r = 0; r < K1P; ++r)
+                            dstk[r] = (r >= XW && r < XW + W) ? k[(r - XW) % W] : (T)0;
+                    } else {
+                        T *dstk = (ax == 0 ? sk1 : sk2) + q * (ax == 0 ? K1P : W);
+#pragma unroll
+                        for (int r = 0; r < W; ++r) dstk[r] = k[r];
+                    }
                 }
                 stt[q * 4 + ax] = t;
             }
@@ -206,7 +216,7 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
                 nk_kernel_rows2<T, W>(pts[j], pts[pitch + j], g, k, kb, t1, t2);
 #pragma unroll
                 for (int r = 0; r < W; ++r) {
-                    sk1[q * W + r] = k[r];
+                    sk1[q * K1P + r] = k[r];
                     sk2[q * W + r] = kb[r];
                 }
                 const int t3 = nk_kernel_row<T, W>(pts[2 * pitch + j], g, k) + h;
@@ -234,7 +244,7 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
                 run_off = row + st.x;
                 e0 = ((warp - st.z) % NW + NW) % NW;
             }
-            const T *k1q = sk1 + q * W;
+            const T *k1q = sk1 + q * K1P;
             const T *k2q = sk2 + q * W;
             T kk[NIT];
             if (XWIN) {
@@ -242,7 +252,7 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
 #pragma unroll
                 for (int it = 0; it < NIT; ++it) {
                     const int kx = la[it] - sh;
-                    kk[it] = (kx >= 0 && kx < W) ? k2q[lb[it]] * k1q[kx] : (T)0;
+                    kk[it] = k2q[lb[it]] * k1q[XW + kx];   // zero padding outside [0, W)
                 }
             } else {
 #pragma unroll

@@ -339,7 +339,7 @@ def run_ours(args, cfg):
     if world > 1:
         dist.barrier()
     step_ms, dom_ms, launches = [], [], 0
-    dom_type = types[0]
+    dom_type = 1 if cfg["type"] == 12 else types[0]   # C5: the type-1 spread dominates
     with Clocks(local) as clk:
         # the timed region is milliseconds long; keep the same load running
         # (untimed) until the sampler has readings on both sides of it

@@ -83,8 +83,8 @@ k_spread_gm(int M, const int32_t *__restrict__ perm, const int32_t *__restrict__
 //    (the f64 kernel is shared-bandwidth bound: 13 x 13 x 16 B x 2 per
 //    point and plane otherwise).
 // The finished bin is merged with native global vector reductions (Eq. 17).
-template <typename T, int W, int NW, int SPLIT>
-__global__ void __launch_bounds__(NW * SPLIT * 32)
+template <typename T, int W, int NW>
+__global__ void __launch_bounds__(NW * 32)
 k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
              const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
              const T *__restrict__ pts, int64_t pitch, const typename cplx<T>::t *__restrict__ c,
@@ -92,10 +92,7 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     typedef typename cplx<T>::t C;
     constexpr bool XWIN = sizeof(T) == 8 && W <= 16;
     constexpr int XW = 16;                      // x-window width (XWIN)
-    // SPLIT warps share a plane group: each takes a contiguous share of the
-    // plane passes (more warps in flight for the 1-CTA-per-SM f64 kernel)
-    constexpr int NIT_ALL = XWIN ? (W + 1) / 2 : (W * W + 31) / 32;
-    constexpr int NIT = (NIT_ALL + SPLIT - 1) / SPLIT;
+    constexpr int NIT = XWIN ? (W + 1) / 2 : (W * W + 31) / 32;
     constexpr int NE = (W + NW - 1) / NW;       // planes per warp per footprint
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *buf = reinterpret_cast<C *>(smem_raw);
@@ -106,9 +103,7 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     T *sk1 = reinterpret_cast<T *>(sst + nbatch);
     T *sk2 = sk1 + nbatch * K1P;
     C *sck3 = reinterpret_cast<C *>(sk2 + nbatch * W);
-    const int lane = threadIdx.x & 31;
-    const int warp = (threadIdx.x >> 5) % NW;            // plane group
-    const int it0 = ((threadIdx.x >> 5) / NW) * NIT;     // first pass of this warp
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x;
     c += blockIdx.y * g.M;          // batched execute: vector blockIdx.y
     fine += blockIdx.y * g.ntot;
@@ -124,13 +119,12 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     bool lok[NIT];
 #pragma unroll
     for (int it = 0; it < NIT; ++it) {
-        const int ig = it0 + it;   // global pass index
         if (XWIN) {
             la[it] = lane & (XW - 1);
-            lb[it] = (lane >> 4) + 2 * ig;
+            lb[it] = (lane >> 4) + 2 * it;
             lok[it] = lb[it] < W;
         } else {
-            const int idx = ig * 32 + lane;
+            const int idx = it * 32 + lane;
             lb[it] = idx / W;
             la[it] = idx - lb[it] * W;
             lok[it] = idx < W * W;
@@ -164,7 +158,7 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
 #pragma unroll
                 for (int it = 0; it < NIT; ++it) {
                     const bool ok = XWIN ? (lok[it] && run_x0 + la[it] < p1)
-                                         : ((SPLIT == 1 && it < NIT - 1) || lok[it]);
+                                         : ((it < NIT - 1) || lok[it]);
                     if (ok) {
                         C *cell = plane + lofs[it];
                         C v = *cell;
@@ -416,12 +410,11 @@ int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
         if (p->S == 0) return NK_OK;
         size_t smem = (size_t)p->max_sub_smem;
         constexpr int NW = nk_sm3_warps(W);
-        constexpr int SPLIT = (sizeof(T) == 8 && W > 8) ? 2 : 1;
-        auto kern = k_spread_sm3<T, W, NW, SPLIT>;
+        auto kern = k_spread_sm3<T, W, NW>;
         NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         int64_t stage_off = (p->max_pad_cells * (int64_t)sizeof(C) + 15) / 16 * 16;
-        kern<<<dim3((unsigned)p->S, p->ntrans), NW * SPLIT * 32, smem, p->stream>>>(
+        kern<<<dim3((unsigned)p->S, p->ntrans), NW * 32, smem, p->stream>>>(
             p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm, (const T *)p->d_pts,
             p->cap_M, (const C *)c, p->geom, (C *)fine, stage_off, nk_sm3_batch(p->prec));
     } else if (p->method == NK_SM && D == 2) {

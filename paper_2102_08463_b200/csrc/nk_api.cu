@@ -64,7 +64,7 @@ void free_plan(nk_plan *p) {
                     p->d_starts, p->d_pts, p->d_alt_keys, p->d_alt_vals, p->d_tile_hist,
                     p->d_scan_tmp, p->d_bad, p->d_nsub_off, p->d_sub_bin, p->d_sub_start,
                     p->d_sub_stop, p->d_in_stage, p->d_out_stage, p->d_vperm_buf,
-                    p->d_pts_alt, p->d_sort_scr};
+                    p->d_pts_alt, p->d_sort_scr, p->d_work};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p->fft_ok) cufftDestroy(p->fft);
@@ -340,6 +340,7 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     NK_ALLOC(p->d_starts, 4 * (p->nbins + 1));
     NK_ALLOC(p->d_nsub_off, 4 * (p->nbins + 1));
     NK_ALLOC(p->d_bad, sizeof(unsigned long long));
+    NK_ALLOC(p->d_work, sizeof(int) * p->ntrans);
 #undef NK_ALLOC
     if (precision == NK_DOUBLE) {
         e = cudaMemcpy(p->d_corr, corr.data(), 8 * corr.size(), cudaMemcpyHostToDevice);

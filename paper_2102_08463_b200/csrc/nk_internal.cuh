@@ -84,6 +84,7 @@ struct nk_plan {
     cufftHandle fft_col;
     bool fft_col_ok;
     void *d_twiddle;        // n_1 complex exp(+2 pi i k / n_1)
+    int *d_work;            // n_trans work counters of the staged interpolation
 
     // points
     int64_t M;

@@ -122,20 +122,26 @@ k_interp_staged(int S, const int32_t *__restrict__ sub_bin, const int32_t *__res
                 const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
                 const T *__restrict__ pts, int64_t pitch,
                 const typename cplx<T>::t *__restrict__ fine, Geom g,
-                typename cplx<T>::t *__restrict__ out, int buf_cells) {
+                typename cplx<T>::t *__restrict__ out, int buf_cells, int *__restrict__ work) {
     typedef typename cplx<T>::t C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int sh_next;
     C *bufs = reinterpret_cast<C *>(smem_raw);
     const int h = g.halo;
     const uint64_t keep = nk_policy_evict_last();
     fine += blockIdx.y * g.ntot;   // batched execute: vector blockIdx.y
     out += blockIdx.y * g.M;
+    work += blockIdx.y;
+    // dynamic scheduling: after its first subproblem a CTA takes the next
+    // unclaimed one from a counter (balanced tails for uneven subproblems)
     int s = blockIdx.x;
     int cur = 0;
+    if (threadIdx.x == 0) sh_next = atomicAdd(work, 1) + gridDim.x;
     if (s < S) stage_padded_bin<T, D>(bufs, fine, g, sub_bin[s]);
     nk_cp_async_commit();
-    for (; s < S; s += gridDim.x) {
-        const int sn = s + gridDim.x;
+    __syncthreads();
+    int sn = sh_next;
+    while (s < S) {
         if (NBUF == 2) {
             if (sn < S) stage_padded_bin<T, D>(bufs + (cur ^ 1) * buf_cells, fine, g, sub_bin[sn]);
             nk_cp_async_commit();
@@ -213,6 +219,10 @@ k_interp_staged(int S, const int32_t *__restrict__ sub_bin, const int32_t *__res
             stage_padded_bin<T, D>(bufs, fine, g, sub_bin[sn]);
             nk_cp_async_commit();
         }
+        s = sn;
+        if (threadIdx.x == 0) sh_next = atomicAdd(work, 1) + gridDim.x;
+        __syncthreads();
+        sn = sh_next;
     }
     nk_cp_async_wait<0>();
 }
@@ -239,10 +249,11 @@ int launch_w(nk_plan *p, const void *fine, void *out, int *launches) {
         int per_sm = 0;
         NK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
         const int64_t grid = std::min<int64_t>(p->S, (int64_t)std::max(per_sm, 1) * nsm);
+        NK_CUDA(cudaMemsetAsync(p->d_work, 0, sizeof(int) * p->ntrans, p->stream));
         kern<<<dim3((unsigned)grid, p->ntrans), threads, smem, p->stream>>>(
             (int)p->S, p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm,
             (const T *)p->d_pts, p->cap_M, (const C *)fine, p->geom, (C *)out,
-            (int)(one / sizeof(C)));
+            (int)(one / sizeof(C)), p->d_work);
     } else {
         const int32_t *perm = p->method == NK_GM ? nullptr : p->d_vperm;
         k_interp_gm<T, D, W><<<dim3((M + 255) / 256, p->ntrans), 256, 0, p->stream>>>(

@@ -58,6 +58,11 @@ class CudaStageOps:
         self.plan.pad_to(modes, self.fine)
         return self.plan.fft_(self.fine, +1)
 
+    def execute_type2(self, modes, out):
+        """The whole type-2 execute on this rank's points (fused pad + FFT +
+        interp, CUDA-graph replay on fixed buffers) once the modes are here."""
+        return self.plan.execute(modes, out)
+
     def interp(self, fine, out=None):
         if out is None:
             out = self.new_values(self.plan.num_points)
@@ -112,6 +117,10 @@ class ShardedPlan:
             return self.ops.fft_deconvolve(fine, out)
         if not self.all_ranks:
             dist.broadcast(inp, src=self.root, group=self.group)
+        if hasattr(self.ops, "execute_type2"):
+            if out is None:
+                out = self.ops.new_values(self.ops.plan.num_points)
+            return self.ops.execute_type2(inp, out)
         fine = self.ops.pad_ifft(inp)
         return self.ops.interp(fine, out)
 

@@ -168,7 +168,13 @@ def cpu_reference(cfg, steps, warmup, sample_cap):
     the M-proportional stage (interp / spread) on `sample` points and scaled
     linearly to M.  Returns (pts_per_sec, cores, sample description)."""
     from oracle import oracle as orc
-    threads = orc.host_threads()
+    # every host core the process may use (torchrun exports OMP_NUM_THREADS=1,
+    # which omp_get_max_threads would report); the oracle takes the count
+    # explicitly
+    try:
+        threads = len(os.sched_getaffinity(0))
+    except AttributeError:
+        threads = os.cpu_count() or orc.host_threads()
     sub = dict(cfg)
     sample = min(cfg["M"], sample_cap)
     sub["M"] = sample

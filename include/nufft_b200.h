@@ -164,6 +164,12 @@ NK_API int nk_fft(nk_plan *plan, void *fine, int direction);
 /* deconvolve_type1 (with the (-1)^{sum k} phase). */
 NK_API int nk_deconv_type1(nk_plan *plan, const void *fine_spectrum, void *modes);
 
+/* fft_fine(forward) followed by deconvolve_type1, in place on `fine`: the
+ * type-1 back half of execute() (2D single precision with n_1 = 2^L: cuFFT
+ * column pass + the fused row-FFT / mode-selection kernel).  Used by the
+ * sharded type-1 path after the fine-grid reduce. */
+NK_API int nk_fft_deconv_type1(nk_plan *plan, void *fine, void *modes);
+
 /* deconvolve_type2 (with the phase): writes every fine cell. */
 NK_API int nk_deconv_type2(nk_plan *plan, const void *modes, void *fine_spectrum);
 

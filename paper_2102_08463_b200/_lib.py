@@ -90,6 +90,7 @@ def lib():
         "nk_fft": (I, [P, P, I]),
         "nk_deconv_type1": (I, [P, P, P]),
         "nk_deconv_type2": (I, [P, P, P]),
+        "nk_fft_deconv_type1": (I, [P, P, P]),
         "nk_stage_times": (I, [P, ctypes.POINTER(ctypes.c_float), I]),
         "nk_last_launch_count": (I, [P]),
         "nk_set_timing": (I, [P, I]),
@@ -106,7 +107,8 @@ EXPORTED = ["nk_tolerance_to_width", "nk_next_smooth", "nk_kernel_fourier", "nk_
             "nk_plan_create", "nk_plan_get_info", "nk_set_stream", "nk_setpts", "nk_execute",
             "nk_destroy", "nk_last_error", "nk_error_index", "nk_get_layout",
             "nk_get_subproblems", "nk_spread", "nk_interp", "nk_fft", "nk_deconv_type1",
-            "nk_deconv_type2", "nk_stage_times", "nk_last_launch_count", "nk_set_timing"]
+            "nk_deconv_type2", "nk_fft_deconv_type1", "nk_stage_times", "nk_last_launch_count",
+            "nk_set_timing"]
 
 
 def check(rc):

@@ -743,6 +743,19 @@ extern "C" int nk_deconv_type1(nk_plan *p, const void *spec, void *modes) {
     return nk_launch_deconv1(p, spec, modes);
 }
 
+extern "C" int nk_fft_deconv_type1(nk_plan *p, void *fine, void *modes) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (p->fused_rows) {
+        NK_CUFFT(cufftExecC2C(p->fft_col, (cufftComplex *)fine, (cufftComplex *)fine,
+                              CUFFT_FORWARD));
+        return nk_launch_rowfft_deconv(p, fine, modes);
+    }
+    rc = do_fft(p, fine, -1);
+    if (rc) return rc;
+    return nk_launch_deconv1(p, fine, modes);
+}
+
 extern "C" int nk_deconv_type2(nk_plan *p, const void *modes, void *spec) {
     int rc = check_plan(p);
     if (rc) return rc;

@@ -51,8 +51,7 @@ class CudaStageOps:
         return self.plan.spread_to(strengths, self.fine)
 
     def fft_deconvolve(self, fine, out):
-        self.plan.fft_(fine, -1)
-        return self.plan.deconvolve_to(fine, out)
+        return self.plan.fft_deconvolve_to(fine, out)
 
     def pad_ifft(self, modes):
         self.plan.pad_to(modes, self.fine)

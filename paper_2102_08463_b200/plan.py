@@ -364,6 +364,16 @@ class TransformPlan:
         _lib.check(self._lib.nk_deconv_type1(self._h, fine_spectrum.data_ptr(), modes.data_ptr()))
         return modes
 
+    def fft_deconvolve_to(self, fine, modes):
+        """Steps 2-3 of type 1 in one call: forward FFT of ``fine`` (in
+        place) and the deconvolution / mode selection into ``modes`` (the
+        fused row-FFT path where the plan has one)."""
+        self._dev(fine, self._batch(self.grid.fine_shape), "fine grid")
+        self._dev(modes, self._batch(self.grid.mode_shape), "modes")
+        self._sync_stream("cuda")
+        _lib.check(self._lib.nk_fft_deconv_type1(self._h, fine.data_ptr(), modes.data_ptr()))
+        return modes
+
     def pad_to(self, modes, fine):
         """Step 1 of type 2: fine <- zero-padded p_k (-1)^{sum k} f_k."""
         self._dev(modes, self._batch(self.grid.mode_shape), "modes")

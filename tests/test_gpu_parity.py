@@ -528,3 +528,33 @@ def test_fused_rowfft_deconv_type1(nk, orc, modes, monkeypatch):
     assert orc.rel_l2_error(got, ref) < 2e-6
     if int(np.prod(modes)) * M <= 4e8:
         assert orc.rel_l2_error(got, orc.direct_type1(pts.astype(np.float64), c, modes)) < 10 * eps
+
+
+@pytest.mark.parametrize("modes,prec", [((256, 200), "single"), ((48, 40), "double"),
+                                         ((16, 12, 10), "single")])
+def test_fft_deconvolve_stage_matches_execute(nk, orc, modes, prec):
+    """The fused type-1 back half exposed for the sharded path
+    (nk_fft_deconv_type1 / plan.fft_deconvolve_to) equals spread + FFT +
+    deconvolution as separate stages and the plan's execute."""
+    import torch
+    eps = 1e-5 if prec == "single" else 1e-9
+    grid = orc.make_grid(modes, eps, prec)
+    rdt = np.float32 if prec == "single" else np.float64
+    pts = orc.gen_points("rand", 3000, grid, 31, rdt)
+    c = orc.gen_strengths(3000, 31).astype(np.complex64 if prec == "single" else np.complex128)
+    p = nk.make_plan(1, modes, eps, "sm", prec)
+    p.set_points(torch.from_numpy(pts).cuda())
+    cd = torch.from_numpy(c).cuda()
+    ref = p.execute(cd)
+    fine = p.new_fine_grid()
+    p.spread_to(cd, fine)
+    out = torch.empty_like(ref)
+    p.fft_deconvolve_to(fine, out)
+    fine2 = p.new_fine_grid()
+    p.spread_to(cd, fine2)
+    p.fft_(fine2, -1)
+    out2 = torch.empty_like(ref)
+    p.deconvolve_to(fine2, out2)
+    tol = 2e-6 if prec == "single" else 1e-13
+    assert orc.rel_l2_error(out.cpu().numpy(), ref.cpu().numpy()) < tol
+    assert orc.rel_l2_error(out2.cpu().numpy(), ref.cpu().numpy()) < tol

@@ -155,10 +155,16 @@ __device__ __forceinline__ void rowfft_stages(float2 *xs, const float2 *__restri
             const int j = threadIdx.x + q * 256;
             if (NB % 256 == 0 || j < NB) {
                 const int k = j & (NS - 1);
+                // one table twiddle per butterfly, powers by recurrence
+                const float2 w1 = NS > 1 ? __ldg(tw + k * TSTEP) : make_float2(1.f, 0.f);
+                float2 w = w1;
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     float2 x = xs[rpad(j + r * NB)];
-                    if (r && NS > 1) x = cmulf(x, __ldg(tw + ((k * r * TSTEP) & (N - 1))));
+                    if (r && NS > 1) {
+                        x = cmulf(x, w);
+                        w = cmulf(w, w1);
+                    }
                     v[q][r] = x;
                 }
             }

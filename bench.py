@@ -553,6 +553,20 @@ def run_ours(args, cfg):
                                 "frac": ach / peak, "traffic": traffic_for(args.config),
                                 "algorithmic_bytes": B, "kernel_ms": dom_avg,
                                 "peak_source": peak_src}
+            # The SM kernels are bound by the shared-memory pipe, not HBM
+            # (DESIGN.md §5): the same launch against the shared-memory
+            # roofline.  Bytes = the footprint cells each point touches in
+            # the padded bin (w^d complex values; read for interp, read +
+            # write for the spread's cell updates), peak = 128 B/clk/SM x
+            # 148 SMs at the max SM clock (architectural, not measured).
+            s = 4 if cfg["prec"] == "single" else 8
+            cells = cfg["M"] * plans[dom_type].params.w ** len(fine)
+            sb = cells * 2 * s * (1 if dom_type == 2 else 2)
+            sh_peak = 148 * 128 * 1965e6 / 1e9
+            line["shared_roofline"] = {
+                "bound": "shared", "achieved": sb / (dom_avg / 1e3) / 1e9, "peak": sh_peak,
+                "unit": "GB/s", "frac": sb / (dom_avg / 1e3) / 1e9 / sh_peak,
+                "bytes": sb, "peak_source": "architectural: 128 B/clk/SM x 148 SMs x 1965 MHz"}
             if stage:
                 line["stage_ms"] = stage
         if e2e:

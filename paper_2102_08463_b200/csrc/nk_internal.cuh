@@ -163,6 +163,17 @@ inline int64_t nk_sm_smem_bytes(int type, int dim, int prec, int w, const int *b
     return b;
 }
 
+// Does the type-2 plan use the x-window group interpolation (K7x,
+// nk_interp.cu: 3D, wide double footprints, padded bin + per-warp staging
+// within the 227 KB opt-in shared memory)?  Its setpts keeps the
+// footprint-start visit order.
+inline int64_t nk_xwin_smem_bytes(int w) { return 16 * 8 * (16 + 3 * w * 8); }
+inline bool nk_interp_xwin(int type, int dim, int prec, int w, int method, int64_t max_sub_smem) {
+    return type == 2 && dim == 3 && prec == NK_DOUBLE && w > 8 && method == NK_SM &&
+           max_sub_smem + nk_xwin_smem_bytes(w) + 1024 <= 227 * 1024 &&
+           !getenv("NK_INTERP_NO_XWIN");
+}
+
 // -------------------------------------------------------------- launchers
 int nk_scan_exclusive(nk_plan *p, const int32_t *in, int32_t *out, int64_t n);
 int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y,

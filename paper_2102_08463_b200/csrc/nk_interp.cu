@@ -227,6 +227,158 @@ k_interp_staged(int S, const int32_t *__restrict__ sub_bin, const int32_t *__res
     nk_cp_async_wait<0>();
 }
 
+// One K7x group of exactly GN points (staged rows at wk[q..q+GN)): every
+// lane reads its window cells (x, bs + 2 i) of all w planes once and
+// accumulates the GN points' k2 k3 weighted sums; k1 and a warp butterfly
+// finish each point.  Cells past the padded row carry k1 = 0 for all points.
+template <typename T, int W, int GN>
+__device__ __forceinline__ void xwin_group(const typename cplx<T>::t *buf, int p1, int p2,
+                                           const int4 *wt, const T *wk, int q, int4 ta, int x,
+                                           int bs, int lane, typename cplx<T>::t *out,
+                                           const int32_t *perm, uint64_t keep) {
+    typedef typename cplx<T>::t C;
+    constexpr int NI = (W + 1) / 2;
+    T kx[GN], k2r[GN][NI];
+#pragma unroll
+    for (int p = 0; p < GN; ++p) {
+        const int sx = x - (wt[q + p].x - ta.x);   // lane's x in point p's row
+        const T *kp = wk + (q + p) * 3 * W;
+        kx[p] = (sx >= 0 && sx < W) ? kp[min(max(sx, 0), W - 1)] : (T)0;
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int b = bs + 2 * i;
+            k2r[p][i] = b < W ? kp[W + min(b, W - 1)] : (T)0;
+        }
+    }
+    C acc[GN];
+#pragma unroll
+    for (int p = 0; p < GN; ++p) acc[p].x = acc[p].y = 0;
+    const C *col = buf + (ta.z * p2 + ta.y) * p1 + min(ta.x + x, p1 - 1);
+    const T *k3 = wk + q * 3 * W + 2 * W;
+#pragma unroll 1
+    for (int e = 0; e < W; ++e) {
+        const C *pl = col + e * p2 * p1;
+        C t[GN];
+#pragma unroll
+        for (int p = 0; p < GN; ++p) t[p].x = t[p].y = 0;
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const C c = pl[min(bs + 2 * i, W - 1) * p1];
+#pragma unroll
+            for (int p = 0; p < GN; ++p) t[p] = nk_fma2(c, k2r[p][i], t[p]);
+        }
+#pragma unroll
+        for (int p = 0; p < GN; ++p) acc[p] = nk_fma2(t[p], k3[p * 3 * W + e], acc[p]);
+    }
+#pragma unroll
+    for (int p = 0; p < GN; ++p) {
+        T vr = acc[p].x * kx[p], vi = acc[p].y * kx[p];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            vr += __shfl_xor_sync(0xffffffffu, vr, o);
+            vi += __shfl_xor_sync(0xffffffffu, vi, o);
+        }
+        if (lane == p) {
+            C v;
+            v.x = vr;
+            v.y = vi;
+            nk_st_keep(out + __ldcs(perm + q + p), v, keep);
+        }
+    }
+}
+
+// K7x: 3D wide-footprint (f64, w > 8) staged interpolation with x-window
+// groups -- the gather counterpart of the f64 spread's register windows.
+// The per-thread gather of K7s reads w^3 x 16 B of shared memory per point
+// (35 KB at w = 13: shared-bandwidth bound, L1 85 %, 22 % bank conflicts).
+// Here a warp takes a GROUP of up to XG consecutive points with the same
+// (t2, t3) footprint start and t1 within 16 - w of the group's first point
+// (footprint-start visit order, K4c, makes them neighbours): its lanes cover
+// a 16-cell x window x 2 rows, read each window cell ONCE per group (one
+// contiguous 256-B row segment per half-warp, no bank conflicts) and
+// accumulate every group point's k2[b] k3[e] weighted sums in registers;
+// the k1[x - t1] factor and a butterfly reduction over the warp finish each
+// point.  Kernel rows are staged per warp, one (point, axis) row per lane.
+template <typename T, int W>
+__global__ void __launch_bounds__(512)
+k_interp_xwin(int S, const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
+              const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
+              const T *__restrict__ pts, int64_t pitch,
+              const typename cplx<T>::t *__restrict__ fine, Geom g,
+              typename cplx<T>::t *__restrict__ out, int buf_cells, int *__restrict__ work) {
+    typedef typename cplx<T>::t C;
+    constexpr int XW = 16, NB = 8, XG = 4, NI = (W + 1) / 2, NWARP = 16;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int sh_next;
+    C *buf = reinterpret_cast<C *>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int4 *wt = reinterpret_cast<int4 *>(buf + buf_cells) + warp * NB;   // (t1, t2, t3)
+    T *wk = reinterpret_cast<T *>(reinterpret_cast<int4 *>(buf + buf_cells) + NWARP * NB) +
+            warp * NB * 3 * W;                                          // k rows [q][axis][r]
+    const int h = g.halo;
+    const uint64_t keep = nk_policy_evict_last();
+    fine += blockIdx.y * g.ntot;
+    out += blockIdx.y * g.M;
+    work += blockIdx.y;
+    const int x = lane & (XW - 1), bs = lane >> 4;
+    int s = blockIdx.x;
+    if (threadIdx.x == 0) sh_next = atomicAdd(work, 1) + gridDim.x;
+    if (s < S) stage_padded_bin<T, 3>(buf, fine, g, sub_bin[s]);
+    nk_cp_async_commit();
+    __syncthreads();
+    int sn = sh_next;
+    while (s < S) {
+        nk_cp_async_wait<0>();
+        __syncthreads();
+        int corner[3];
+        nk_bin_corner(sub_bin[s], g, corner);
+        const int p1 = min(g.m[0], g.n[0] - corner[0]) + 2 * h;
+        const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
+        const int j0 = sub_start[s], j1 = sub_stop[s];
+        const int chunk = (j1 - j0 + NWARP - 1) / NWARP;
+        const int a0 = j0 + warp * chunk, a1 = min(j1, a0 + chunk);
+        for (int base = a0; base < a1; base += NB) {
+            const int nb = min(NB, a1 - base);
+            __syncwarp();
+            if (lane < 3 * nb) {
+                const int q = lane / 3, ax = lane - 3 * q;
+                T k[W];
+                const int t = nk_kernel_row<T, W>(__ldcs(pts + ax * pitch + base + q), g, k) + h;
+#pragma unroll
+                for (int r = 0; r < W; ++r) wk[(q * 3 + ax) * W + r] = k[r];
+                reinterpret_cast<int *>(wt)[q * 4 + ax] = t;
+            }
+            __syncwarp();
+            for (int q = 0; q < nb;) {   // warp-uniform group walk
+                const int4 ta = wt[q];
+                int gn = 1;
+                while (gn < XG && q + gn < nb) {
+                    const int4 tb = wt[q + gn];
+                    if (tb.y != ta.y || tb.z != ta.z || (unsigned)(tb.x - ta.x) > XW - W) break;
+                    ++gn;
+                }
+                switch (gn) {
+                case 1: xwin_group<T, W, 1>(buf, p1, p2, wt, wk, q, ta, x, bs, lane, out, perm + base, keep); break;
+                case 2: xwin_group<T, W, 2>(buf, p1, p2, wt, wk, q, ta, x, bs, lane, out, perm + base, keep); break;
+                case 3: xwin_group<T, W, 3>(buf, p1, p2, wt, wk, q, ta, x, bs, lane, out, perm + base, keep); break;
+                default: xwin_group<T, W, 4>(buf, p1, p2, wt, wk, q, ta, x, bs, lane, out, perm + base, keep); break;
+                }
+                q += gn;
+            }
+        }
+        __syncthreads();   // buffer free
+        if (sn < S) {
+            stage_padded_bin<T, 3>(buf, fine, g, sub_bin[sn]);
+            nk_cp_async_commit();
+        }
+        s = sn;
+        if (threadIdx.x == 0) sh_next = atomicAdd(work, 1) + gridDim.x;
+        __syncthreads();
+        sn = sh_next;
+    }
+    nk_cp_async_wait<0>();
+}
+
 template <typename T, int D, int W>
 int launch_w(nk_plan *p, const void *fine, void *out, int *launches) {
     typedef typename cplx<T>::t C;
@@ -237,6 +389,26 @@ int launch_w(nk_plan *p, const void *fine, void *out, int *launches) {
         int nsm = 0;
         NK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device));
         const size_t one = (size_t)p->max_sub_smem;   // padded bin, 16-B rounded
+        if constexpr (D == 3 && sizeof(T) == 8 && W > 8) {
+            const size_t xsm = one + nk_xwin_smem_bytes(W);
+            if (nk_interp_xwin(p->type, p->dim, p->prec, p->w, p->method, p->max_sub_smem)) {
+                auto kern = k_interp_xwin<T, W>;
+                NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)xsm));
+                int per_sm = 0;
+                NK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, xsm));
+                const int64_t grid =
+                    std::min<int64_t>(p->S, (int64_t)std::max(per_sm, 1) * nsm);
+                NK_CUDA(cudaMemsetAsync(p->d_work, 0, sizeof(int) * p->ntrans, p->stream));
+                kern<<<dim3((unsigned)grid, p->ntrans), 512, xsm, p->stream>>>(
+                    (int)p->S, p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm,
+                    (const T *)p->d_pts, p->cap_M, (const C *)fine, p->geom, (C *)out,
+                    (int)(one / sizeof(C)), p->d_work);
+                NK_LAUNCH_CHECK();
+                ++*launches;
+                return NK_OK;
+            }
+        }
         // double-buffer when two padded bins leave room for a useful occupancy
         const bool two = 2 * one <= 100 * 1024;
         const size_t smem = two ? 2 * one : one;

@@ -767,8 +767,16 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
             rc = order_by_start(p);   // composite key would exceed 32 bits
             if (rc) return rc;
         } else if (p->type == 2) {
-            bool interleave = !composite && p->prec == NK_DOUBLE;
-            if (composite) {
+            const bool xwin = nk_interp_xwin(p->type, p->dim, p->prec, p->w, p->method,
+                                             p->max_sub_smem);
+            bool interleave = !composite && p->prec == NK_DOUBLE && !xwin;
+            if (xwin) {
+                // K7x groups neighbours in footprint-start order
+                if (!composite) {
+                    rc = order_by_start(p);
+                    if (rc) return rc;
+                }
+            } else if (composite) {
                 unsigned long long *d_sq = p->d_bad;   // reused: setpts' error flag is read
                 NK_CUDA(cudaMemsetAsync(d_sq, 0, sizeof(unsigned long long), st));
                 k_sum_sq<<<std::min(blocks_for(nbins, 256), 1184u), 256, 0, st>>>(

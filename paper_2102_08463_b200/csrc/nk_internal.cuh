@@ -167,7 +167,13 @@ inline int64_t nk_sm_smem_bytes(int type, int dim, int prec, int w, const int *b
 // nk_interp.cu: 3D, wide double footprints, padded bin + per-warp staging
 // within the 227 KB opt-in shared memory)?  Its setpts keeps the
 // footprint-start visit order.
-inline int64_t nk_xwin_smem_bytes(int w) { return 16 * 8 * (16 + 3 * w * 8); }
+#ifndef NK_XWIN_NB
+#define NK_XWIN_NB 10  // points staged per warp batch (K7x; 8: 12.5, 10: 11.9 ms at C5)
+#endif
+#ifndef NK_XWIN_G
+#define NK_XWIN_G 4    // max points per K7x group (2 / 3 / 6 / 8: 12.7 / 12.1 / 12.9 / 14.5 ms)
+#endif
+inline int64_t nk_xwin_smem_bytes(int w) { return 16 * NK_XWIN_NB * (16 + 3 * w * 8); }
 inline bool nk_interp_xwin(int type, int dim, int prec, int w, int method, int64_t max_sub_smem) {
     return type == 2 && dim == 3 && prec == NK_DOUBLE && w > 8 && method == NK_SM &&
            max_sub_smem + nk_xwin_smem_bytes(w) + 1024 <= 227 * 1024 &&

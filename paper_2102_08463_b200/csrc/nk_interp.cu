@@ -287,6 +287,24 @@ __device__ __forceinline__ void xwin_group(const typename cplx<T>::t *buf, int p
     }
 }
 
+// exact-size group instantiation for gn in [GN, XG]
+template <typename T, int W, int GN, int XG>
+__device__ __forceinline__ void xwin_dispatch(int gn, const typename cplx<T>::t *buf, int p1,
+                                              int p2, const int4 *wt, const T *wk, int q,
+                                              int4 ta, int x, int bs, int lane,
+                                              typename cplx<T>::t *out, const int32_t *perm,
+                                              uint64_t keep) {
+    if constexpr (GN == XG) {
+        xwin_group<T, W, GN>(buf, p1, p2, wt, wk, q, ta, x, bs, lane, out, perm, keep);
+    } else {
+        if (gn == GN)
+            xwin_group<T, W, GN>(buf, p1, p2, wt, wk, q, ta, x, bs, lane, out, perm, keep);
+        else
+            xwin_dispatch<T, W, GN + 1, XG>(gn, buf, p1, p2, wt, wk, q, ta, x, bs, lane, out,
+                                            perm, keep);
+    }
+}
+
 // K7x: 3D wide-footprint (f64, w > 8) staged interpolation with x-window
 // groups -- the gather counterpart of the f64 spread's register windows.
 // The per-thread gather of K7s reads w^3 x 16 B of shared memory per point
@@ -307,7 +325,7 @@ k_interp_xwin(int S, const int32_t *__restrict__ sub_bin, const int32_t *__restr
               const typename cplx<T>::t *__restrict__ fine, Geom g,
               typename cplx<T>::t *__restrict__ out, int buf_cells, int *__restrict__ work) {
     typedef typename cplx<T>::t C;
-    constexpr int XW = 16, NB = 8, XG = 4, NI = (W + 1) / 2, NWARP = 16;
+    constexpr int XW = 16, NB = NK_XWIN_NB, XG = NK_XWIN_G, NWARP = 16;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int sh_next;
     C *buf = reinterpret_cast<C *>(smem_raw);
@@ -357,12 +375,8 @@ k_interp_xwin(int S, const int32_t *__restrict__ sub_bin, const int32_t *__restr
                     if (tb.y != ta.y || tb.z != ta.z || (unsigned)(tb.x - ta.x) > XW - W) break;
                     ++gn;
                 }
-                switch (gn) {
-                case 1: xwin_group<T, W, 1>(buf, p1, p2, wt, wk, q, ta, x, bs, lane, out, perm + base, keep); break;
-                case 2: xwin_group<T, W, 2>(buf, p1, p2, wt, wk, q, ta, x, bs, lane, out, perm + base, keep); break;
-                case 3: xwin_group<T, W, 3>(buf, p1, p2, wt, wk, q, ta, x, bs, lane, out, perm + base, keep); break;
-                default: xwin_group<T, W, 4>(buf, p1, p2, wt, wk, q, ta, x, bs, lane, out, perm + base, keep); break;
-                }
+                xwin_dispatch<T, W, 1, XG>(gn, buf, p1, p2, wt, wk, q, ta, x, bs, lane, out,
+                                            perm + base, keep);
                 q += gn;
             }
         }

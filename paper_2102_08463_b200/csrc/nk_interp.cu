@@ -13,6 +13,11 @@
 
 namespace {
 
+#ifndef NK_XWIN_EU
+#define NK_XWIN_EU 1
+#endif
+constexpr int kXwinEU = NK_XWIN_EU;   // K7x plane-loop unroll
+
 template <typename T, int D, int W>
 __device__ __forceinline__ typename cplx<T>::t
 gather_global(const typename cplx<T>::t *__restrict__ fine, const Geom &g, int s1, int s2,
@@ -255,7 +260,7 @@ __device__ __forceinline__ void xwin_group(const typename cplx<T>::t *buf, int p
     for (int p = 0; p < GN; ++p) acc[p].x = acc[p].y = 0;
     const C *col = buf + (ta.z * p2 + ta.y) * p1 + min(ta.x + x, p1 - 1);
     const T *k3 = wk + q * 3 * W + 2 * W;
-#pragma unroll 1
+#pragma unroll kXwinEU
     for (int e = 0; e < W; ++e) {
         const C *pl = col + e * p2 * p1;
         C t[GN];

@@ -485,6 +485,32 @@ def test_two_stage_start_order_fallback(nk, orc):
     assert np.array_equal(perm, lay.perm) and np.array_equal(starts, lay.starts)
 
 
+@pytest.mark.parametrize("dist,eps", [("rand", 1e-12), ("cluster", 1e-9), ("rand", 1e-11)])
+def test_xwin_interp_matches_per_thread_gather(nk, orc, dist, eps, monkeypatch):
+    """3D double type 2 with w > 8 gathers by x-window groups (K7x: a warp
+    serves up to 4 start-adjacent points from one read of each window cell).
+    Must match the per-thread staged gather (K7s, NK_INTERP_NO_XWIN=1) to
+    rounding, in both its start and its non-start visit orders, and direct
+    sums (10 eps)."""
+    modes, M = (24, 20, 16), 6000
+    grid = orc.make_grid(modes, eps, "double")
+    pts = orc.gen_points(dist, M, grid, 31, np.float64)
+    rng = np.random.default_rng(5)
+    f = rng.standard_normal(modes[::-1]) + 1j * rng.standard_normal(modes[::-1])
+    p = nk.make_plan(2, modes, eps, "sm", "double")
+    p.set_points(pts)
+    got = p.execute(f)
+    monkeypatch.setenv("NK_INTERP_NO_XWIN", "1")
+    q = nk.make_plan(2, modes, eps, "sm", "double")
+    q.set_points(pts)
+    ref = q.execute(f)
+    assert orc.rel_l2_error(got, ref) < 1e-14
+    # K7x on the K7s visit order (set_points without, execute with K7x)
+    monkeypatch.delenv("NK_INTERP_NO_XWIN")
+    assert orc.rel_l2_error(q.execute(f), ref) < 1e-14
+    assert orc.rel_l2_error(got, orc.direct_type2(pts, f, modes)) < 10 * eps
+
+
 @pytest.mark.parametrize("modes", [(128, 96), (512, 300), (1024, 40)])
 def test_fused_pad_rowfft_type2(nk, orc, modes, monkeypatch):
     """2D single-precision type 2 with n_1 = 2^L runs K9 fused with the row

@@ -173,7 +173,10 @@ inline int64_t nk_sm_smem_bytes(int type, int dim, int prec, int w, const int *b
 #ifndef NK_XWIN_G
 #define NK_XWIN_G 4    // max points per K7x group (2 / 3 / 6 / 8: 12.7 / 12.1 / 12.9 / 14.5 ms)
 #endif
-inline int64_t nk_xwin_smem_bytes(int w) { return 16 * NK_XWIN_NB * (16 + 3 * w * 8); }
+#ifndef NK_XWIN_WARPS
+#define NK_XWIN_WARPS 16  // K7x warps per CTA (one CTA per SM)
+#endif
+inline int64_t nk_xwin_smem_bytes(int w) { return NK_XWIN_WARPS * NK_XWIN_NB * (16 + 3 * w * 8); }
 inline bool nk_interp_xwin(int type, int dim, int prec, int w, int method, int64_t max_sub_smem) {
     return type == 2 && dim == 3 && prec == NK_DOUBLE && w > 8 && method == NK_SM &&
            max_sub_smem + nk_xwin_smem_bytes(w) + 1024 <= 227 * 1024 &&

@@ -323,14 +323,14 @@ __device__ __forceinline__ void xwin_dispatch(int gn, const typename cplx<T>::t 
 // the k1[x - t1] factor and a butterfly reduction over the warp finish each
 // point.  Kernel rows are staged per warp, one (point, axis) row per lane.
 template <typename T, int W>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(32 * NK_XWIN_WARPS)
 k_interp_xwin(int S, const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
               const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
               const T *__restrict__ pts, int64_t pitch,
               const typename cplx<T>::t *__restrict__ fine, Geom g,
               typename cplx<T>::t *__restrict__ out, int buf_cells, int *__restrict__ work) {
     typedef typename cplx<T>::t C;
-    constexpr int XW = 16, NB = NK_XWIN_NB, XG = NK_XWIN_G, NWARP = 16;
+    constexpr int XW = 16, NB = NK_XWIN_NB, XG = NK_XWIN_G, NWARP = NK_XWIN_WARPS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int sh_next;
     C *buf = reinterpret_cast<C *>(smem_raw);
@@ -363,8 +363,8 @@ k_interp_xwin(int S, const int32_t *__restrict__ sub_bin, const int32_t *__restr
         for (int base = a0; base < a1; base += NB) {
             const int nb = min(NB, a1 - base);
             __syncwarp();
-            if (lane < 3 * nb) {
-                const int q = lane / 3, ax = lane - 3 * q;
+            for (int v = lane; v < 3 * nb; v += 32) {
+                const int q = v / 3, ax = v - 3 * q;
                 T k[W];
                 const int t = nk_kernel_row<T, W>(__ldcs(pts + ax * pitch + base + q), g, k) + h;
 #pragma unroll
@@ -415,11 +415,11 @@ int launch_w(nk_plan *p, const void *fine, void *out, int *launches) {
                 NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)xsm));
                 int per_sm = 0;
-                NK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, xsm));
+                NK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * NK_XWIN_WARPS, xsm));
                 const int64_t grid =
                     std::min<int64_t>(p->S, (int64_t)std::max(per_sm, 1) * nsm);
                 NK_CUDA(cudaMemsetAsync(p->d_work, 0, sizeof(int) * p->ntrans, p->stream));
-                kern<<<dim3((unsigned)grid, p->ntrans), 512, xsm, p->stream>>>(
+                kern<<<dim3((unsigned)grid, p->ntrans), 32 * NK_XWIN_WARPS, xsm, p->stream>>>(
                     (int)p->S, p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm,
                     (const T *)p->d_pts, p->cap_M, (const C *)fine, p->geom, (C *)out,
                     (int)(one / sizeof(C)), p->d_work);

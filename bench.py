@@ -1,20 +1,26 @@
 #!/usr/bin/env python
 """Benchmark: NU points/sec (exec, device-timed) for the BASELINE configs.
 
-Default workload = BASELINE.json configs[1] ("C2"): 2D type-2 single
-precision, N = 1024 x 1024 (fine 2048 x 2048), M = 1e7 uniform points,
-eps = 1e-5.  A step = one execute() (pad -> cuFFT inverse -> interp) with
-the points already set (the paper's "exec").
+Default workload = BASELINE.json configs[3] ("C4"), the largest single-GPU
+configuration (BASELINE's metric is not quoted on one config, so the
+headline is the largest): 3D double precision, N = 256^3 (fine 512^3,
+w = 13), M = 1e8 uniform points, eps = 1e-12.  A step = one type-1 execute
+(spread -> cuFFT forward -> deconvolution) plus one type-2 execute (pad ->
+cuFFT inverse -> interp) on the same points, both with the points already
+set (the paper's "exec"); value = 2 M / step time.
 
-  python bench.py [--gpus N --steps K --warmup W] [--config c2] [--method sm]
+  python bench.py [--gpus N --steps K --warmup W] [--config c4] [--method sm]
   python bench.py --impl reference ...   # the reference algorithm on host cores
 
-Multi-GPU (torchrun, one process per GPU, NCCL): type-2 configs shard the
-points (each rank owns its own M points, weak scaling) against a replicated
-fine grid; rank 0's modes are broadcast every step (the real exchange).
-Type-1 configs shard points and sum the per-rank fine grids with an NCCL
-reduce before the root's FFT + deconvolution.  c5 runs independent
-replicas (no collective).  Times are CUDA-event device times, max over ranks.
+Multi-GPU (torchrun, one process per GPU, NCCL).  --scaling strong (the C4
+default) splits the config's M points across ranks (contiguous slices of
+the input order); --scaling weak (the default for the other configs) gives
+every rank its own M points.  Type-1 transforms spread each rank's points
+into its own fine grid and sum the grids with an NCCL reduce before the
+root's FFT + deconvolution; type-2 transforms broadcast the root's modes
+and interpolate each rank's points on the replicated grid.  c5 runs
+independent replicas (no collective).  Times are CUDA-event device times,
+max over ranks.
 """
 
 from __future__ import annotations
@@ -64,10 +70,24 @@ CONFIGS = {
                  prec="double", desc="C4 3D type-1 f64 N=256^3 M=1e8 uniform eps=1e-12"),
     "c4t2": dict(type=2, modes=(256, 256, 256), M=100_000_000, dist="rand", eps=1e-12,
                  prec="double", desc="C4 3D type-2 f64 N=256^3 M=1e8 uniform eps=1e-12"),
+    "c4": dict(type=21, modes=(256, 256, 256), M=100_000_000, dist="rand", eps=1e-12,
+               prec="double", scaling="strong", cpu_sample=300_000,
+               desc="C4 3D type-1 + type-2 f64 N=256^3 M=1e8 uniform eps=1e-12"),
     "c5": dict(type=12, modes=(128, 128, 128), M=10_000_000, dist="rand", eps=1e-12,
-               prec="double",
+               prec="double", cpu_sample=300_000,
                desc="C5 3D type-2 then type-1 f64 N=128^3 M=1e7 per rank, eps=1e-12"),
 }
+for _k in ("c4t1", "c4t2"):
+    CONFIGS[_k]["scaling"] = "strong"
+    CONFIGS[_k]["cpu_sample"] = 300_000
+for _k in ("c5t1", "c5t2"):
+    CONFIGS[_k]["cpu_sample"] = 300_000
+
+
+def config_types(cfg):
+    """Transforms per step, in execution order (c5: type 2 then type 1,
+    the M-TIP slicing/merging pair; c4: type 1 then type 2)."""
+    return {12: [2, 1], 21: [1, 2]}.get(cfg["type"], [cfg["type"]])
 METRIC = "NU points/sec (exec, device-timed) at tol eps, 2D/3D type 1/2, at 1/2/4/8 B200"
 L2_FLUSH_BYTES = 256 << 20
 
@@ -81,12 +101,25 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def algorithmic_bytes(cfg, fine):
+def algorithmic_bytes(cfg, fine, M=None):
     """SURVEY.md §8(d) per-kernel bytes of the dominant kernel
     (spread for type 1, interp for type 2): M (d+2) s + 2 n_tot s."""
     d = len(cfg["modes"])
     s = 4 if cfg["prec"] == "single" else 8
-    return cfg["M"] * (d + 2) * s + 2 * int(np.prod(fine)) * s
+    M = cfg["M"] if M is None else M
+    return M * (d + 2) * s + 2 * int(np.prod(fine)) * s
+
+
+def fp64_peak():
+    """Measured FP64 FMA throughput (TFLOP/s) from profiles/fp64_peak.json
+    (scripts/fp64_peak.cu on a B200 of this pool), else the architectural
+    148 SMs x 64 DFMA/clk x 2 flops x 1.965 GHz."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fh:
+            j = json.load(fh)
+        return float(j["fp64_fma_tflops"]), "measured (profiles/fp64_peak.json, scripts/fp64_peak.cu)"
+    except Exception:
+        return 148 * 64 * 2 * 1.965e9 / 1e12, "architectural: 148 SMs x 64 DFMA/clk x 2 x 1965 MHz"
 
 
 class Clocks:
@@ -176,10 +209,20 @@ def cpu_reference(cfg, steps, warmup, sample_cap):
     except AttributeError:
         threads = os.cpu_count() or orc.host_threads()
     sub = dict(cfg)
+    if sample_cap is None:
+        sample_cap = cfg.get("cpu_sample", cfg["M"])
     sample = min(cfg["M"], sample_cap)
     sub["M"] = sample
     grid, pts, f, c = make_inputs(sub, 0)
-    types = [2, 1] if cfg["type"] == 12 else [cfg["type"]]
+    box = None
+    if sample < cfg["M"] and cfg["dist"] == "rand":
+        # keep the full-M point density: the sample fills a sub-box of the
+        # domain (side (sample / M)^(1/d) of 2 pi) instead of thinning the
+        # whole grid, so the SM spread's per-bin setup / merge is amortised
+        # over as many points per bin as at full size
+        box = (sample / cfg["M"]) ** (1.0 / len(cfg["modes"]))
+        pts = (-np.pi + (pts + np.pi) * box).astype(pts.dtype)
+    types = config_types(cfg)
     plans = {}
     for t in types:
         p = orc.OraclePlan(t, cfg["modes"], cfg["eps"], "sm" if t == 1 else "gmsort",
@@ -213,11 +256,17 @@ def cpu_reference(cfg, steps, warmup, sample_cap):
             times.append(tot)
     t_step = float(np.median(times))
     npts = cfg["M"] * len(types)
-    desc = (f"oracle C port (nufftkit algorithm: {'GM-sort interp' if 2 in types else ''}"
-            f"{' + ' if len(types) == 2 else ''}{'SM spread' if 1 in types else ''}, "
-            f"scipy.fft) on {threads} host threads; M-proportional stage timed on "
-            f"{sample} of {cfg['M']} points and scaled; pad/FFT/deconv at full size; "
-            f"median of {steps}")
+    what = " + ".join({2: "GM-sort interp", 1: "SM spread"}[t] for t in types)
+    if sample == cfg["M"]:
+        size = f"every stage at full size (M = {cfg['M']})"
+    else:
+        size = (f"SUBSAMPLED: the M-proportional stage timed on {sample} of {cfg['M']} "
+                f"points and scaled linearly"
+                + (f" (the sample fills a {box:.3f}^{len(cfg['modes'])} fraction of the "
+                   f"domain at the full-M density)" if box else "")
+                + "; pad/FFT/deconv at full size")
+    desc = (f"oracle C port (nufftkit algorithm: {what}, scipy.fft) on {threads} host "
+            f"threads; {size}; median of {steps}")
     return npts / t_step, threads, desc, t_step
 
 
@@ -228,7 +277,8 @@ def run_reference(args, cfg):
     v, cores, desc, t_step = cpu_reference(cfg, args.steps, args.warmup, args.cpu_sample)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "NU pts/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": cfg.get("scaling", "weak"),
             "vs_baseline": None, "dtype": "f32" if cfg["prec"] == "single" else "f64",
             "data": "synthetic (seeded numpy: uniform / cluster / gauss points, U[0,1)^2 "
                     "complex strengths)",
@@ -264,9 +314,23 @@ def run_ours(args, cfg):
             dist.init_process_group(backend)
 
     import paper_2102_08463_b200 as nk
+    from paper_2102_08463_b200.dist import CudaStageOps, ReplicaPlan, ShardedPlan, shard_bounds
 
-    grid, pts, f_host, c_host = make_inputs(cfg, args.seed, rank)
-    types = [2, 1] if cfg["type"] == 12 else [cfg["type"]]
+    types = config_types(cfg)
+    scaling = args.scaling or cfg.get("scaling", "weak")
+    replicas = cfg["type"] == 12               # C5: independent M-TIP replicas
+    sharded = world > 1 and not replicas
+    if scaling == "strong" and world > 1:
+        # the config's M points split across ranks: same inputs as N = 1
+        grid, pts, f_host, c_host = make_inputs(cfg, args.seed, 0)
+        lo, hi = shard_bounds(cfg["M"], world, rank)
+        pts = np.ascontiguousarray(pts[lo:hi])
+        c_host = np.ascontiguousarray(c_host[lo:hi])
+        total_pts = cfg["M"]
+    else:
+        grid, pts, f_host, c_host = make_inputs(cfg, args.seed, rank)
+        total_pts = world * cfg["M"]
+    M = pts.shape[0]
     plans = {}
     pts_dev = torch.from_numpy(pts).to(dev)
     setpts_ms = {}
@@ -288,18 +352,14 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     f_dev = torch.from_numpy(f_host).to(dev)
     c_dev = torch.from_numpy(c_host).to(dev)
-    out_t2 = torch.empty(cfg["M"], dtype=c_dev.dtype, device=dev)
-    out_t1 = torch.empty(cfg["modes"][::-1], dtype=c_dev.dtype, device=dev)
+    out_dev = {2: torch.empty(M, dtype=c_dev.dtype, device=dev),
+               1: torch.empty(cfg["modes"][::-1], dtype=c_dev.dtype, device=dev)}
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-    from paper_2102_08463_b200.dist import CudaStageOps, ReplicaPlan, ShardedPlan
-    sharded = world > 1 and cfg["type"] in (1, 2)
     runners = {}
     for t in types:
-        if sharded:
-            runners[t] = ShardedPlan(CudaStageOps(plans[t]), t, root=0)
-        else:
-            runners[t] = ReplicaPlan(plans[t])   # world 1, or independent replicas (c5)
-    dom_in_step = []
+        runners[t] = (ShardedPlan(CudaStageOps(plans[t]), t, root=0) if sharded
+                      else ReplicaPlan(plans[t]))
+    spread_ev = []
 
     def step():
         """One exec per transform in the config; returns this library's
@@ -310,7 +370,7 @@ def run_ours(args, cfg):
         for t in types:
             r = runners[t]
             if isinstance(r, ReplicaPlan):
-                r.execute(f_dev if t == 2 else c_dev, out_t2 if t == 2 else out_t1)
+                r.execute(f_dev if t == 2 else c_dev, out_dev[t])
                 launches += plans[t].last_launch_count()
             elif t == 1:
                 ev_a = torch.cuda.Event(enable_timing=True)
@@ -318,19 +378,17 @@ def run_ours(args, cfg):
                 ev_a.record()
                 fine = r.ops.spread(c_dev)
                 ev_b.record()
-                dom_in_step.append((ev_a, ev_b))
+                spread_ev.append((ev_a, ev_b))
                 if backend == "nccl":
                     dist.reduce(fine, dst=0)
                 else:
                     dist.all_reduce(fine)
                 launches += 1
                 if rank == 0:
-                    r.ops.fft_deconvolve(fine, out_t1)
+                    r.ops.fft_deconvolve(fine, out_dev[1])
                     launches += 1
             else:
-                # NCCL broadcast of the modes, then this rank's whole type-2
-                # execute (fused pad + FFT + interp, graph replay)
-                r.execute(f_dev, out_t2)
+                r.execute(f_dev, out_dev[2])
                 launches += plans[t].last_launch_count()
         return launches
 
@@ -339,11 +397,12 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    step_ms, dom_ms, launches = [], [], 0
-    dom_type = 1 if cfg["type"] == 12 else types[0]   # C5: the type-1 spread dominates
+    launches = 0
+    kern_ms = {t: [] for t in types}
+    stage = {}
     with Clocks(local) as clk:
-        # the timed region is milliseconds long; keep the same load running
-        # (untimed) until the sampler has readings on both sides of it
+        # the timed region can be milliseconds long; keep the same load
+        # running (untimed) until the sampler has readings on both sides
         t_pre = time.time()
         soak = 0.0 if os.environ.get("NK_BENCH_NO_CLOCKS") else 5.0
 
@@ -368,7 +427,7 @@ def run_ours(args, cfg):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        dom_in_step.clear()
+        spread_ev.clear()
         evs = []
         for _ in range(args.steps):
             flush.fill_(1.0)                       # L2 flush between timed steps
@@ -382,47 +441,46 @@ def run_ours(args, cfg):
         if world > 1:
             dist.barrier()
         step_ms = [a.elapsed_time(b) for a, b in evs]
-        if sharded and dom_type == 1:
-            dom_ms = [a.elapsed_time(b) for a, b in dom_in_step]
-            dom_in_step.clear()
-        # dominant-kernel time for the roofline: same steps again with the
-        # plan's per-stage CUDA events on (direct launches, no graph replay;
+        if sharded and 1 in types:
+            kern_ms[1] = [a.elapsed_time(b) for a, b in spread_ev]
+        spread_ev.clear()
+        # per-kernel times for the rooflines: the same steps again with the
+        # plans' per-stage CUDA events on (direct launches, no graph replay;
         # every rank runs the same steps, collectives included)
-        stage = None
-        if not (sharded and dom_type == 1):
-            plans[dom_type].set_timing(True)
-            for _ in range(args.steps):
-                flush.fill_(1.0)
-                torch.cuda.synchronize()
-                step()
-                torch.cuda.synchronize()
-                st = plans[dom_type].stage_times()
-                dom_ms.append(st["interp" if dom_type == 2 else "spread"])
-            stage = st
-            plans[dom_type].set_timing(False)
+        timed = [t for t in types if not (sharded and t == 1)]
+        for t in timed:
+            plans[t].set_timing(True)
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            step()
+            torch.cuda.synchronize()
+            for t in timed:
+                st = plans[t].stage_times()
+                kern_ms[t].append(st["interp" if t == 2 else "spread"])
+                stage[f"type{t}"] = st
+        for t in timed:
+            plans[t].set_timing(False)
+        spread_ev.clear()
         t_post = time.time()
         soak_while(lambda: len(clk.lines) < n_pre + 3 and time.time() - t_post < soak)
     tot_ms = float(np.sum(step_ms))
-    dom_avg = float(np.mean(dom_ms)) if dom_ms else None
     if world > 1:
         t = torch.tensor([tot_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
 
-    # ---- e2e: the public API with pinned host buffers, copies inside the timing.
-    # Single GPU / replicas: plan.execute(host in, host out) through the C-ABI
-    # (H2D + exec + D2H, synchronous).  Sharded: each rank copies its inputs
-    # H2D, runs the sharded step (collective included) and reads its result
-    # back D2H.
-    e2e = None
-    pin_in = {}
+    # ---- e2e (headline): the public API with pinned host buffers, copies
+    # inside the timing.  Unsharded: plan.execute(host in, host out) through
+    # the C-ABI (H2D + exec + D2H, synchronous) for every transform of the
+    # step.  Sharded: each rank copies its inputs H2D, runs the sharded step
+    # (collectives included) and reads its result back D2H.
+    pin_in, pin_out = {}, {}
     for t in types:
         src = f_host if t == 2 else c_host
-        b = torch.empty(src.shape, dtype=c_dev.dtype, pin_memory=True)
-        b.numpy()[...] = src
-        pin_in[t] = b
-    pin_out = {2: torch.empty(cfg["M"], dtype=c_dev.dtype, pin_memory=True),
-               1: torch.empty(cfg["modes"][::-1], dtype=c_dev.dtype, pin_memory=True)}
+        pin_in[t] = torch.empty(src.shape, dtype=c_dev.dtype, pin_memory=True)
+        pin_in[t].numpy()[...] = src
+        pin_out[t] = torch.empty(out_dev[t].shape, dtype=c_dev.dtype, pin_memory=True)
 
     def e2e_step():
         if not sharded:
@@ -430,21 +488,16 @@ def run_ours(args, cfg):
                 plans[t].execute(pin_in[t].numpy(), pin_out[t].numpy())
             return
         for t in types:
-            if t == 2:
-                f_dev.copy_(pin_in[2], non_blocking=True)
-            else:
-                c_dev.copy_(pin_in[1], non_blocking=True)
+            (f_dev if t == 2 else c_dev).copy_(pin_in[t], non_blocking=True)
         step()
         for t in types:
-            if t == 2:
-                pin_out[2].copy_(out_t2, non_blocking=True)
-            elif rank == 0:
-                pin_out[1].copy_(out_t1, non_blocking=True)
+            if t == 2 or rank == 0:
+                pin_out[t].copy_(out_dev[t], non_blocking=True)
         torch.cuda.synchronize()
 
     for _ in range(max(1, args.warmup)):
         e2e_step()
-    dom_in_step.clear()
+    spread_ev.clear()
     e2e_s = []
     for _ in range(args.steps):
         flush.fill_(1.0)
@@ -454,34 +507,32 @@ def run_ours(args, cfg):
         t0 = time.perf_counter()
         e2e_step()
         e2e_s.append(time.perf_counter() - t0)
-    dom_in_step.clear()
+    spread_ev.clear()
     e2e_t = float(np.sum(e2e_s))
     if world > 1:
         t = torch.tensor([e2e_t], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_t = float(t.item())
-    if True:
-        csz = c_dev.element_size()
-        h2d = sum((int(np.prod(cfg["modes"])) if t == 2 else cfg["M"]) * csz for t in types)
-        d2h = sum((cfg["M"] if t == 2 else int(np.prod(cfg["modes"]))) * csz for t in types)
-        e2e = {"value": world * cfg["M"] * len(types) * args.steps / e2e_t, "unit": "NU pts/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "mode": "one synchronous execute(host in, host out) per step"}
+    csz = c_dev.element_size()
+    nmodes = int(np.prod(cfg["modes"]))
+    h2d = sum((nmodes if t == 2 else M) * csz for t in types)
+    d2h = sum((M if t == 2 else nmodes) * csz for t in types)
+    e2e = {"value": total_pts * len(types) * args.steps / e2e_t, "unit": "NU pts/s",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "mode": "one synchronous execute(host in, host out) per transform per step "
+                   "through the C-ABI (pinned host buffers; H2D + exec + D2H timed)"}
 
-    # ---- streamed e2e (single transform, unsharded): the same public
-    # execute() on device buffers, with every step's H2D input copy and D2H
-    # result copy on their own streams so step i's D2H overlaps step i+1's
-    # H2D and compute (PCIe is full duplex).  K steps, each with its own
-    # copies, timed from the first H2D to the last D2H.  The per-step working
-    # set (~240 MB at C2) exceeds L2, so no flush between steps.
-    if not sharded and len(types) == 1:
-        t = types[0]
-        p = plans[t]
-        src_pin = pin_in[t]
-        dins = [torch.empty(src_pin.shape, dtype=c_dev.dtype, device=dev) for _ in range(2)]
-        oshape = (cfg["M"],) if t == 2 else tuple(cfg["modes"][::-1])
-        douts = [torch.empty(oshape, dtype=c_dev.dtype, device=dev) for _ in range(2)]
-        pouts = [torch.empty(oshape, dtype=c_dev.dtype, pin_memory=True) for _ in range(2)]
+    # ---- streamed variant (unsharded): the same public execute() on device
+    # buffers, every step's H2D input copy and D2H result copy on their own
+    # streams so step i's D2H overlaps step i+1's H2D and compute (PCIe is
+    # full duplex).  Reported beside the synchronous headline.
+    if not sharded:
+        dins = {t: [torch.empty(pin_in[t].shape, dtype=c_dev.dtype, device=dev)
+                    for _ in range(2)] for t in types}
+        douts = {t: [torch.empty(out_dev[t].shape, dtype=c_dev.dtype, device=dev)
+                     for _ in range(2)] for t in types}
+        pouts = {t: [torch.empty(out_dev[t].shape, dtype=c_dev.dtype, pin_memory=True)
+                     for _ in range(2)] for t in types}
         s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
         ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "cmp", "out")}
 
@@ -490,18 +541,21 @@ def run_ours(args, cfg):
                 b = i & 1
                 with torch.cuda.stream(s_in):
                     if i >= 2:
-                        s_in.wait_event(ev["cmp"][b])      # step i-2 done reading dins[b]
-                    dins[b].copy_(src_pin, non_blocking=True)
+                        s_in.wait_event(ev["cmp"][b])      # step i-2 done reading dins
+                    for t in types:
+                        dins[t][b].copy_(pin_in[t], non_blocking=True)
                     ev["in"][b].record(s_in)
                 with torch.cuda.stream(s_cmp):
                     s_cmp.wait_event(ev["in"][b])
                     if i >= 2:
-                        s_cmp.wait_event(ev["out"][b])     # D2H of step i-2 done with douts[b]
-                    p.execute(dins[b], douts[b])
+                        s_cmp.wait_event(ev["out"][b])     # D2H of step i-2 done with douts
+                    for t in types:
+                        plans[t].execute(dins[t][b], douts[t][b])
                     ev["cmp"][b].record(s_cmp)
                 with torch.cuda.stream(s_out):
                     s_out.wait_event(ev["cmp"][b])
-                    pouts[b].copy_(douts[b], non_blocking=True)
+                    for t in types:
+                        pouts[t][b].copy_(douts[t][b], non_blocking=True)
                     ev["out"][b].record(s_out)
             torch.cuda.synchronize()
 
@@ -511,71 +565,112 @@ def run_ours(args, cfg):
         st_t = time.perf_counter() - t0
         # same inputs as the synchronous e2e: results agree up to the float
         # reduction order of the spread's atomics
-        a_res = pouts[(args.steps - 1) & 1].numpy().reshape(-1)
-        b_res = pin_out[t].numpy().reshape(-1)
-        ok = float(np.linalg.norm(a_res - b_res)) <= 1e-5 * float(np.linalg.norm(b_res))
-        e2e_sync = e2e
-        e2e = {"value": cfg["M"] * args.steps / st_t, "unit": "NU pts/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "mode": "streamed: per-step H2D / execute / D2H on three streams, double-"
-                       "buffered (copies of step i+1 overlap step i)",
-               "matches_sync_result": bool(ok),
-               "sync": e2e_sync}
+        ok = True
+        for t in types:
+            a_res = pouts[t][(args.steps - 1) & 1].numpy().reshape(-1)
+            b_res = pin_out[t].numpy().reshape(-1)
+            ok &= float(np.linalg.norm(a_res - b_res)) <= 1e-5 * float(np.linalg.norm(b_res))
+        e2e["streamed"] = {
+            "value": M * len(types) * args.steps / st_t, "unit": "NU pts/s",
+            "mode": "per-step H2D / execute / D2H on three streams, double-buffered "
+                    "(copies of step i+1 overlap step i)",
+            "matches_sync_result": bool(ok)}
+        for t in types:
+            dins[t] = douts[t] = pouts[t] = None
+
+    # per-kernel averages (max over ranks)
+    kern_avg = {}
+    for t in types:
+        v = float(np.mean(kern_ms[t])) if kern_ms[t] else 0.0
+        if world > 1:
+            x = torch.tensor([v], device=dev)
+            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+            v = float(x.item())
+        if v > 0:
+            kern_avg[t] = v
 
     if rank == 0:
+        dom_type = max(kern_avg, key=kern_avg.get) if kern_avg else types[0]
         fine = plans[dom_type].grid.fine
+        w = plans[dom_type].params.w
         peak, peak_src = peaks()
+        par = ("1 GPU" if world == 1 else
+               f"{world} independent replicas" if replicas else
+               f"{world} GPUs, {scaling} scaling: points sharded, type-1 fine grids "
+               "NCCL-reduced to rank 0 / type-2 modes NCCL-broadcast")
         line = {
             "metric": METRIC,
-            "value": world * cfg["M"] * len(types) * args.steps / (tot_ms / 1e3),
+            "value": total_pts * len(types) * args.steps / (tot_ms / 1e3),
             "unit": "NU pts/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": scaling if world > 1 else cfg.get("scaling", "weak"),
             "vs_baseline": None, "dtype": "f32" if cfg["prec"] == "single" else "f64",
             "data": "synthetic (seeded numpy: uniform / cluster / gauss points, U[0,1)^2 "
                     "complex strengths), inputs resident in HBM",
-            "config": {"workload": cfg["desc"] + (f", per rank x {world}" if world > 1 else ""),
+            "config": {"workload": cfg["desc"] + (f", per rank x {world}"
+                                                  if world > 1 and scaling == "weak" else ""),
+                       "transforms_per_step": [f"type{t}" for t in types],
                        "method": plans[dom_type].method,
-                       "fine": list(fine), "w": plans[dom_type].params.w,
-                       "bin_dims": list(plans[dom_type].bin_dims),
+                       "fine": list(fine), "w": w,
+                       "bin_dims": {f"type{t}": list(plans[t].bin_dims) for t in types},
                        "l2": "flushed between timed steps (256 MiB write)",
-                       "parallelism": ("1 GPU" if world == 1 else
-                                       f"{world} GPUs: points sharded, type-1 fine grids "
-                                       "NCCL-reduced / type-2 modes NCCL-broadcast"
-                                       if sharded else f"{world} independent replicas")},
+                       "parallelism": par},
             "gpu_launches": launches,
             "setpts_ms": setpts_ms,
         }
-        if dom_avg:
-            B = algorithmic_bytes(cfg, fine)
-            ach = B / (dom_avg / 1e3) / 1e9
-            line["roofline"] = {"bound": "hbm", "kernel": "interp" if dom_type == 2 else "spread",
+        # setpts against its SURVEY §8(d) bytes: coords read + 3 M int32
+        # (key write / re-read / perm write) + permuted coords written
+        d = len(cfg["modes"])
+        s = 4 if cfg["prec"] == "single" else 8
+        sp_bytes = M * d * s * 2 + 3 * M * 4
+        sp_ms = setpts_ms[f"type{types[0]}"]
+        line["setpts_roofline"] = {"bound": "hbm", "algorithmic_bytes": sp_bytes,
+                                   "achieved": sp_bytes / (sp_ms / 1e3) / 1e9, "peak": peak,
+                                   "unit": "GB/s",
+                                   "frac": sp_bytes / (sp_ms / 1e3) / 1e9 / peak}
+        if kern_avg:
+            dom_ms = kern_avg[dom_type]
+            B = algorithmic_bytes(cfg, fine, M)
+            ach = B / (dom_ms / 1e3) / 1e9
+            line["roofline"] = {"bound": "hbm",
+                                "kernel": "interp" if dom_type == 2 else "spread",
                                 "achieved": ach, "peak": peak, "unit": "GB/s",
                                 "frac": ach / peak, "traffic": traffic_for(args.config),
-                                "algorithmic_bytes": B, "kernel_ms": dom_avg,
+                                "algorithmic_bytes": B, "kernel_ms": dom_ms,
+                                "kernel_ms_by_type": {f"type{t}": v for t, v in kern_avg.items()},
                                 "peak_source": peak_src}
+            if cfg["prec"] == "double":
+                # the f64 spread / interp are FP64-pipe bound: w^d cell updates
+                # per point, each a complex x real FMA (2 DFMA = 4 flops)
+                fpk, fpk_src = fp64_peak()
+                flops = 4.0 * M * w ** d
+                line["fp64_roofline"] = {
+                    "bound": "fp64", "flops_per_point": 4 * w ** d, "peak": fpk,
+                    "unit": "TFLOP/s", "peak_source": fpk_src,
+                    "by_kernel": {("interp" if t == 2 else "spread"): {
+                        "achieved": flops / (v / 1e3) / 1e12,
+                        "frac": flops / (v / 1e3) / 1e12 / fpk, "kernel_ms": v}
+                        for t, v in kern_avg.items()}}
             # The SM kernels are bound by the shared-memory pipe, not HBM
             # (DESIGN.md §5): the same launch against the shared-memory
             # roofline.  Bytes = the footprint cells each point touches in
             # the padded bin (w^d complex values; read for interp, read +
             # write for the spread's cell updates), peak = 128 B/clk/SM x
             # 148 SMs at the max SM clock (architectural, not measured).
-            s = 4 if cfg["prec"] == "single" else 8
-            cells = cfg["M"] * plans[dom_type].params.w ** len(fine)
+            cells = M * w ** d
             sb = cells * 2 * s * (1 if dom_type == 2 else 2)
             sh_peak = 148 * 128 * 1965e6 / 1e9
             line["shared_roofline"] = {
-                "bound": "shared", "achieved": sb / (dom_avg / 1e3) / 1e9, "peak": sh_peak,
-                "unit": "GB/s", "frac": sb / (dom_avg / 1e3) / 1e9 / sh_peak,
+                "bound": "shared", "achieved": sb / (dom_ms / 1e3) / 1e9, "peak": sh_peak,
+                "unit": "GB/s", "frac": sb / (dom_ms / 1e3) / 1e9 / sh_peak,
                 "bytes": sb, "peak_source": "architectural: 128 B/clk/SM x 148 SMs x 1965 MHz"}
             if dom_type == 1:
                 line["shared_roofline"]["note"] = (
                     "bytes = the reference SM scheme's per-point cell read-modify-writes; "
-                    "register run accumulation skips most of them on clustered points, "
-                    "so frac can exceed 1 there")
+                    "register accumulation skips most of them, so frac can exceed 1")
             if stage:
                 line["stage_ms"] = stage
-        if e2e:
-            line["e2e"] = e2e
+        line["e2e"] = e2e
         line["clocks"] = clk.summary()
         if world == 1 and not args.no_cpu_baseline:
             v, cores, desc, _ = cpu_reference(cfg, 2, 1, args.cpu_sample)
@@ -605,12 +700,17 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c4")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default=None,
+                    help="multi-GPU: split the config's M across ranks (strong) or give "
+                         "every rank its own M (weak); default per config (c4 strong)")
     ap.add_argument("--method", default=None)
     ap.add_argument("--msub", type=int, default=None, help="max subproblem size override")
     ap.add_argument("--bins", default=None, help="bin dims override, e.g. 16,16")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--cpu-sample", type=int, default=2_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=None,
+                    help="points of the CPU baseline's M-proportional stage (default: the "
+                         "full M for c1-c3, a flagged subsample for c4 / c5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -58,11 +58,22 @@ extern "C" {
 typedef struct nk_plan nk_plan;
 
 typedef struct {
-    int method;          /* NK_METHOD_DEFAULT: SM for type 1, GM-sort for type 2 */
-    int bin_dims[3];     /* 0 = default (32,32) / (16,16,2), binsort.py:34-35 */
-    int max_subproblem;  /* 0 = default 1024, binsort.py:38 */
+    int method;          /* NK_METHOD_DEFAULT: SM for both types.  Type 1 follows
+                            SPEC.md:170; for type 2 SPEC.md:170 says GM-sort, this
+                            library deviates and picks the shared-memory staged
+                            gather ("sm", measured faster on B200) */
+    int bin_dims[3];     /* 0 = default.  GM-sort plans: the reference's (32,32) /
+                            (16,16,2) (binsort.py:34-35).  SM plans: B200-tuned shapes
+                            -- type 1: 2D (16,8), 3D f32 (4,4,4), 3D f64 (16,8,4);
+                            type 2: 2D (32,32), 3D f32 (16,16,4), 3D f64 (8,8,8);
+                            halved along axes 1/2 while the padded bin exceeds
+                            shared memory */
+    int max_subproblem;  /* 0 = default.  The reference default is 1024
+                            (binsort.py:38); SM plans use 128 for 2D type 1, 1024
+                            for 3D type 1 and 4096 for type 2 */
     int64_t fine[3];     /* 0 = sizing rule n_i = next_smooth(max(2N_i, 2w)) */
-    int device;          /* -1 = current device */
+    int device;          /* -1 = current device.  Every call on the plan runs on this
+                            device and restores the caller's current device */
     void *stream;        /* cudaStream_t, NULL = default stream */
     int timing;          /* nonzero: record per-stage CUDA events (nk_stage_times) */
     int n_trans;         /* vectors per execute (cufinufft ntransf); 0 or 1 = one.  The
@@ -101,6 +112,13 @@ NK_API int64_t nk_next_smooth(int64_t n);
 /* kernel.py:149-173 kernel_fourier: phi_hat(xi) by 100-node Gauss-Legendre
  * after z = sin(theta).  Host arrays. */
 NK_API int nk_kernel_fourier(double beta, const double *xi, int64_t n, double *out);
+
+/* kernel.py:181-205 build_correction_factors: writes the (N_d, ..., N_1)
+ * table (2/w)^d / prod_i phi_hat(alpha_i k_i) over centered k_i into host
+ * memory `out` (float for NK_SINGLE, double for NK_DOUBLE).  modes / alpha
+ * are axis 1 first.  NK_ERR_VALUE when phi_hat underflows (kernel.py:195-199). */
+NK_API int nk_correction_factors(double beta, int w, int dim, const int64_t *modes,
+                                 const double *alpha, int precision, void *out);
 
 /* ---- plan lifecycle -------- */
 

@@ -526,6 +526,30 @@ void or_direct_type1(int64_t M, int d, const double *pts, const double *c,
     }
 }
 
+/* direct_type1 at selected modes only (SPEC.md:473-481 restricted to the
+ * integer wave vectors kv (nk, d)): spot checks at geometries whose full
+ * direct sum is out of reach (BASELINE C3-C5). */
+void or_direct_type1_at(int64_t M, int d, const double *pts, const double *c, int64_t nk,
+                        const int64_t *kv, int nthreads, double *out) {
+    if (nthreads < 1) nthreads = 1;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+    for (int64_t o = 0; o < nk; ++o) {
+        double k1 = (double)kv[o * d], k2 = (double)kv[o * d + 1];
+        double k3 = d == 3 ? (double)kv[o * d + 2] : 0.0;
+        nsum re = {0, 0}, im = {0, 0};
+        for (int64_t j = 0; j < M; ++j) {
+            double ph = k1 * pts[j * d] + k2 * pts[j * d + 1];
+            if (d == 3) ph += k3 * pts[j * d + 2];
+            double s = sin(ph), co = cos(ph);
+            double cr = c[2 * j], ci = c[2 * j + 1];
+            nadd(&re, cr * co + ci * s);
+            nadd(&im, ci * co - cr * s);
+        }
+        out[2 * o] = re.s + re.c;
+        out[2 * o + 1] = im.s + im.c;
+    }
+}
+
 /* direct_type2: c_j = sum_k f_k exp(+i k.x_j). */
 void or_direct_type2(int64_t M, int d, const double *pts, const double *modes,
                      const int64_t *N, int nthreads, double *c) {

@@ -84,6 +84,7 @@ def lib():
         L.or_deconv_type2.argtypes = [I, P, P, P, P, I, P]
         L.or_direct_type1.argtypes = [I64, I, P, P, P, I, P]
         L.or_direct_type2.argtypes = [I64, I, P, P, P, I, P]
+        L.or_direct_type1_at.argtypes = [I64, I, P, P, I64, P, I, P]
         L.or_max_threads.restype = I
         _lib = L
     return _lib
@@ -500,6 +501,19 @@ def direct_type1(points, strengths, modes, workers=0):
                           _p(np.asarray(modes, np.int64)), workers or host_threads(),
                           _p(out))
     return out.reshape(-1)
+
+
+def direct_type1_at(points, strengths, kvecs, workers=0):
+    """SPEC.md:473-481 at the integer wave vectors ``kvecs`` (n, d), axis 1
+    first: f_k = sum_j c_j e^{-i k.x_j}, compensated."""
+    kv = np.ascontiguousarray(kvecs, np.int64)
+    d = kv.shape[1]
+    pts = _pts64(points, d)
+    c = np.ascontiguousarray(strengths, np.complex128).reshape(-1)
+    out = np.empty(kv.shape[0], np.complex128)
+    lib().or_direct_type1_at(pts.shape[0], d, _p(pts), _p(c), kv.shape[0], _p(kv),
+                             workers or host_threads(), _p(out))
+    return out
 
 
 def direct_type2(points, fmodes, modes, workers=0):

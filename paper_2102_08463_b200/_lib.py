@@ -74,6 +74,7 @@ def lib():
                                       ctypes.POINTER(D), ctypes.POINTER(I)]),
         "nk_next_smooth": (I64, [I64]),
         "nk_kernel_fourier": (I, [D, P, I64, P]),
+        "nk_correction_factors": (I, [D, I, I, P, P, I, P]),
         "nk_default_opts": (None, [ctypes.POINTER(NkOpts)]),
         "nk_plan_create": (I, [I, I, P, D, I, ctypes.POINTER(NkOpts), PP]),
         "nk_plan_get_info": (I, [P, ctypes.POINTER(NkPlanInfo)]),
@@ -103,7 +104,8 @@ def lib():
     return L
 
 
-EXPORTED = ["nk_tolerance_to_width", "nk_next_smooth", "nk_kernel_fourier", "nk_default_opts",
+EXPORTED = ["nk_tolerance_to_width", "nk_next_smooth", "nk_kernel_fourier",
+            "nk_correction_factors", "nk_default_opts",
             "nk_plan_create", "nk_plan_get_info", "nk_set_stream", "nk_setpts", "nk_execute",
             "nk_destroy", "nk_last_error", "nk_error_index", "nk_get_layout",
             "nk_get_subproblems", "nk_spread", "nk_interp", "nk_fft", "nk_deconv_type1",

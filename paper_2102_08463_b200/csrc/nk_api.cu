@@ -77,6 +77,26 @@ void free_plan(nk_plan *p) {
     delete p;
 }
 
+// Every entry point that touches the device runs on the plan's device and
+// restores the caller's current device on return (a single process may
+// drive plans on several GPUs, PAPER.md:1617-1618 gpu_device_id).
+struct DevGuard {
+    int prev = -1;
+    bool switched = false;
+    explicit DevGuard(int dev) {
+        if (dev < 0 || cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            return;
+        }
+        if (prev != dev) switched = cudaSetDevice(dev) == cudaSuccess;
+        if (!switched) cudaGetLastError();
+    }
+    ~DevGuard() {
+        if (switched) cudaSetDevice(prev);
+    }
+};
+#define NK_DEVICE_GUARD(p) DevGuard _nk_dev_guard((p)->device)
+
 int check_plan(const nk_plan *p) {
     if (!p) {
         nk_set_error("null plan");
@@ -211,16 +231,22 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
         return NK_ERR_VALUE;
     }
 
-    // device
+    // device: the plan lives on opts.device (or the current one); the
+    // caller's current device is restored on return
     if (opts.device >= 0) {
-        cudaError_t e = cudaSetDevice(opts.device);
-        if (e != cudaSuccess) {
-            nk_set_error(std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+        int ndev = 0;
+        cudaGetDeviceCount(&ndev);
+        cudaGetLastError();
+        if (opts.device >= ndev) {
+            nk_set_error("invalid CUDA device " + std::to_string(opts.device));
             delete p;
-            return NK_ERR_CUDA;
+            return NK_ERR_VALUE;
         }
+        p->device = opts.device;
+    } else {
+        cudaGetDevice(&p->device);
     }
-    cudaGetDevice(&p->device);
+    DevGuard dev_guard(p->device);
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
 
@@ -446,6 +472,7 @@ extern "C" int nk_plan_get_info(const nk_plan *p, nk_plan_info *info) {
 extern "C" int nk_set_stream(nk_plan *p, void *stream) {
     int rc = check_plan(p);
     if (rc) return rc;
+    NK_DEVICE_GUARD(p);
     p->stream = (cudaStream_t)stream;
     NK_CUFFT(cufftSetStream(p->fft, p->stream));
     if (p->fft_col_ok) NK_CUFFT(cufftSetStream(p->fft_col, p->stream));
@@ -456,6 +483,7 @@ extern "C" int nk_setpts(nk_plan *p, int64_t M, int coord_prec, const void *x, c
                          const void *z, int64_t stride) {
     int rc = check_plan(p);
     if (rc) return rc;
+    NK_DEVICE_GUARD(p);
     if (M < 0 || M >= INT32_MAX) {
         nk_set_error("number of points must be in [0, 2^31-1), got " + std::to_string(M));
         return NK_ERR_VALUE;
@@ -605,6 +633,7 @@ static int execute_graph(nk_plan *p, const void *in, void *out) {
 extern "C" int nk_execute(nk_plan *p, const void *in, void *out) {
     int rc = check_plan(p);
     if (rc) return rc;
+    NK_DEVICE_GUARD(p);
     if (!p->have_points) {
         nk_set_error("execute called before set_points");
         return NK_ERR_STATE;
@@ -641,6 +670,7 @@ extern "C" int nk_execute(nk_plan *p, const void *in, void *out) {
 
 extern "C" int nk_destroy(nk_plan *p) {
     if (!p) return NK_OK;
+    NK_DEVICE_GUARD(p);
     if (p->stream) cudaStreamSynchronize(p->stream);
     free_plan(p);
     return NK_OK;
@@ -652,6 +682,7 @@ extern "C" int nk_get_layout(const nk_plan *p, int32_t *point_bins, int32_t *cou
                              int32_t *starts, int32_t *perm) {
     int rc = check_plan(p);
     if (rc) return rc;
+    NK_DEVICE_GUARD(p);
     if (!p->have_points) {
         nk_set_error("no points set");
         return NK_ERR_STATE;
@@ -681,6 +712,7 @@ extern "C" int nk_get_subproblems(const nk_plan *p, int32_t *bin_ids, int32_t *s
                                   int32_t *slice_stops, int32_t *offsets, int32_t *padded) {
     int rc = check_plan(p);
     if (rc) return rc;
+    NK_DEVICE_GUARD(p);
     if (p->method != NK_SM) {
         nk_set_error("subproblems exist only for sm plans");
         return NK_ERR_STATE;
@@ -712,6 +744,7 @@ extern "C" int nk_get_subproblems(const nk_plan *p, int32_t *bin_ids, int32_t *s
 extern "C" int nk_spread(nk_plan *p, const void *strengths, void *fine) {
     int rc = check_plan(p);
     if (rc) return rc;
+    NK_DEVICE_GUARD(p);
     if (!p->have_points) {
         nk_set_error("spread called before set_points");
         return NK_ERR_STATE;
@@ -723,6 +756,7 @@ extern "C" int nk_spread(nk_plan *p, const void *strengths, void *fine) {
 extern "C" int nk_interp(nk_plan *p, const void *fine, void *out) {
     int rc = check_plan(p);
     if (rc) return rc;
+    NK_DEVICE_GUARD(p);
     if (!p->have_points) {
         nk_set_error("interp called before set_points");
         return NK_ERR_STATE;
@@ -734,18 +768,21 @@ extern "C" int nk_interp(nk_plan *p, const void *fine, void *out) {
 extern "C" int nk_fft(nk_plan *p, void *fine, int direction) {
     int rc = check_plan(p);
     if (rc) return rc;
+    NK_DEVICE_GUARD(p);
     return do_fft(p, fine, direction);
 }
 
 extern "C" int nk_deconv_type1(nk_plan *p, const void *spec, void *modes) {
     int rc = check_plan(p);
     if (rc) return rc;
+    NK_DEVICE_GUARD(p);
     return nk_launch_deconv1(p, spec, modes);
 }
 
 extern "C" int nk_fft_deconv_type1(nk_plan *p, void *fine, void *modes) {
     int rc = check_plan(p);
     if (rc) return rc;
+    NK_DEVICE_GUARD(p);
     if (p->fused_rows) {
         NK_CUFFT(cufftExecC2C(p->fft_col, (cufftComplex *)fine, (cufftComplex *)fine,
                               CUFFT_FORWARD));
@@ -759,12 +796,14 @@ extern "C" int nk_fft_deconv_type1(nk_plan *p, void *fine, void *modes) {
 extern "C" int nk_deconv_type2(nk_plan *p, const void *modes, void *spec) {
     int rc = check_plan(p);
     if (rc) return rc;
+    NK_DEVICE_GUARD(p);
     return nk_launch_deconv2(p, modes, spec);
 }
 
 extern "C" int nk_stage_times(nk_plan *p, float *ms, int n) {
     int rc = check_plan(p);
     if (rc) return rc;
+    NK_DEVICE_GUARD(p);
     if (!p->timing || !p->ev_ok) {
         nk_set_error("plan was not created with timing enabled");
         return NK_ERR_STATE;
@@ -788,6 +827,7 @@ extern "C" int nk_stage_times(nk_plan *p, float *ms, int n) {
 extern "C" int nk_set_timing(nk_plan *p, int on) {
     int rc = check_plan(p);
     if (rc) return rc;
+    NK_DEVICE_GUARD(p);
     if (on && !p->ev_ok) {
         for (auto &ev : p->ev) NK_CUDA(cudaEventCreate(&ev));
         p->ev_ok = true;

@@ -133,3 +133,56 @@ extern "C" int nk_kernel_fourier(double beta, const double *xi, int64_t n, doubl
     }
     return NK_OK;
 }
+
+// kernel.py:181-205 build_correction_factors: the full (N_d, ..., N_1) table
+// p_k = (2/w)^d / prod_i phi_hat(alpha_i k_i), k_i centered (kernel.py:176-178),
+// with the reference's product order (axis d outermost, multiplied down to
+// axis 1, kernel.py:201-203) and the cast to the plan's real dtype
+// (kernel.py:205).  Host output; the CUDA path uses per-axis factors instead.
+extern "C" int nk_correction_factors(double beta, int w, int dim, const int64_t *modes,
+                                     const double *alpha, int precision, void *out) {
+    if (dim < 1 || dim > 3 || !modes || !alpha || !out || w < 1 ||
+        (precision != NK_SINGLE && precision != NK_DOUBLE)) {
+        nk_set_error("invalid correction-factor arguments");
+        return NK_ERR_VALUE;
+    }
+    // np.finfo(real dtype).tiny * 100 (kernel.py:190)
+    const double floor_v = (precision == NK_DOUBLE ? 2.2250738585072014e-308
+                                                   : 1.1754943508222875e-38) * 100;
+    std::vector<std::vector<double>> ft(dim);
+    int64_t total = 1;
+    for (int i = 0; i < dim; ++i) {
+        const int64_t Ni = modes[i];
+        if (Ni < 0) {
+            nk_set_error("invalid mode count");
+            return NK_ERR_VALUE;
+        }
+        std::vector<double> xi(Ni);
+        for (int64_t k = 0; k < Ni; ++k) xi[k] = alpha[i] * (double)(k - Ni / 2);
+        ft[i].resize(Ni);
+        nk_kernel_fourier_host(beta, xi.data(), Ni, ft[i].data());
+        for (int64_t k = 0; k < Ni; ++k)
+            if (!(ft[i][k] > floor_v)) {   // kernel.py:195-199
+                nk_set_error("kernel Fourier transform underflowed on axis " +
+                             std::to_string(i + 1) + "; correction factors would overflow");
+                return NK_ERR_VALUE;
+            }
+        total *= Ni;
+    }
+    const double c = pow(2.0 / w, (double)dim);
+    const int64_t N1 = modes[0], N2 = dim > 1 ? modes[1] : 1, N3 = dim > 2 ? modes[2] : 1;
+    int64_t o = 0;
+    for (int64_t k3 = 0; k3 < N3; ++k3)
+        for (int64_t k2 = 0; k2 < N2; ++k2)
+            for (int64_t k1 = 0; k1 < N1; ++k1, ++o) {
+                double prod;
+                if (dim == 1) prod = ft[0][k1];
+                else if (dim == 2) prod = ft[1][k2] * ft[0][k1];
+                else prod = (ft[2][k3] * ft[1][k2]) * ft[0][k1];
+                const double v = c / prod;
+                if (precision == NK_DOUBLE) ((double *)out)[o] = v;
+                else ((float *)out)[o] = (float)v;
+            }
+    (void)total;
+    return NK_OK;
+}

@@ -84,17 +84,21 @@ k_fold_keys(int M, const TC *__restrict__ x, const TC *__restrict__ y,
 // starts[b] = first sorted position with key >= b (length nbins + 1, so
 // starts[nbins] = M) from the bin-sorted keys; counts = adjacent
 // differences.  Identical to bincount + exclusive cumsum (binsort.py:149-151).
+// One thread per bin, lower_bound over the sorted keys: O(nbins log M),
+// independent of how the points cluster (empty-bin runs cost nothing).
 __global__ void __launch_bounds__(256)
 k_bin_starts(int M, int nbins, const int32_t *__restrict__ skeys, int sb,
              int32_t *__restrict__ starts) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= M) return;
-    // (composite keys carry the bin in the bits above sb)
-    const int k = (int)((unsigned)skeys[i] >> sb);
-    const int kp = i ? (int)((unsigned)skeys[i - 1] >> sb) : -1;
-    for (int b = kp + 1; b <= k; ++b) starts[b] = i;
-    if (i == M - 1)
-        for (int b = k + 1; b <= nbins; ++b) starts[b] = M;
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nbins) return;
+    // (composite keys carry the bin in the bits above sb; sorted as unsigned)
+    int lo = 0, hi = M;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((int)((unsigned)__ldg(skeys + mid) >> sb) < b) lo = mid + 1;
+        else hi = mid;
+    }
+    starts[b] = lo;
 }
 
 // sum_b counts[b]^2 (point-weighted bin density for the visit-order choice)
@@ -623,7 +627,11 @@ static int order_by_start(nk_plan *p) {
     const int64_t M = p->M;
     cudaStream_t st = p->stream;
     int32_t *scr = p->d_sort_scr;
-    int32_t *k0 = scr, *v0 = scr + M, *k1 = scr + 2 * M, *v1 = scr + 3 * M;
+    // quarters of the scratch at cap_M offsets (a multiple of 16 elements):
+    // every buffer stays 16-byte aligned for the radix passes' int4 loads,
+    // whatever the parity of M
+    const int64_t q = p->cap_M;
+    int32_t *k0 = scr, *v0 = scr + q, *k1 = scr + 2 * q, *v1 = scr + 3 * q;
     const unsigned nb = blocks_for(M, 256);
     if (p->prec == NK_DOUBLE)
         k_start_keys<double><<<nb, 256, 0, st>>>((int)M, p->d_keys, (const double *)p->d_pts,
@@ -699,8 +707,9 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
         }
         if (rc) return rc;
         p->sorted = true;
-        k_bin_starts<<<blocks_for(M, 256), 256, 0, st>>>((int)M, nbins, p->d_keys,
-                                                         composite ? sb : 0, p->d_starts);
+        k_bin_starts<<<blocks_for(nbins + 1, 256), 256, 0, st>>>((int)M, nbins, p->d_keys,
+                                                                 composite ? sb : 0,
+                                                                 p->d_starts);
         k_counts_from_starts<<<blocks_for(nbins, 256), 256, 0, st>>>(nbins, p->d_starts,
                                                                      p->d_counts);
         NK_LAUNCH_CHECK();
@@ -793,11 +802,25 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
                 rc = order_by_start(p);   // composite key would exceed 32 bits
                 if (rc) return rc;
             }
+            if (interleave && 4 * ((int64_t)p->msub + 1) + 1024 > 227 * 1024)
+                interleave = false;   // bucket table would not fit in shared memory
             if (interleave) {
                 // in: current visit order; out: scratch-backed visit order
                 int32_t *vout = composite ? p->d_sort_scr : p->d_vperm_buf;
                 int32_t *scr = composite ? p->d_sort_scr + p->cap_M : p->d_alt_keys;
+                // round_start[] holds one int per point of the largest
+                // subproblem: past the 48 KB default the kernel opts in
                 size_t smem = 4 * ((size_t)p->msub + 1);
+                if (smem > 48 * 1024) {
+                    if (p->prec == NK_DOUBLE)
+                        NK_CUDA(cudaFuncSetAttribute(k_refine_interleave<double>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)smem));
+                    else
+                        NK_CUDA(cudaFuncSetAttribute(k_refine_interleave<float>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)smem));
+                }
                 if (p->prec == NK_DOUBLE)
                     k_refine_interleave<double><<<(unsigned)p->S, 256, smem, st>>>(
                         p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm,

@@ -69,10 +69,12 @@ class CudaStageOps:
 
     def new_modes(self):
         p = self.plan
-        return torch.empty(p.grid.mode_shape, dtype=self.fine.dtype, device=self.fine.device)
+        return torch.empty(p._batch(p.grid.mode_shape), dtype=self.fine.dtype,
+                           device=self.fine.device)
 
     def new_values(self, n):
-        return torch.empty(n, dtype=self.fine.dtype, device=self.fine.device)
+        return torch.empty(self.plan._batch((n,)), dtype=self.fine.dtype,
+                           device=self.fine.device)
 
 
 class ShardedPlan:
@@ -99,6 +101,9 @@ class ShardedPlan:
         self.root = root
         self.all_ranks = all_ranks
         self.rank = dist.get_rank(group)
+        # ``root`` is a rank of ``group``; torch's reduce(dst=) / broadcast(src=)
+        # take global ranks
+        self.root_global = root if group is None else dist.get_global_rank(group, root)
 
     def execute(self, inp, out=None):
         """type 1: inp = this rank's strengths -> modes (root / all ranks,
@@ -109,13 +114,13 @@ class ShardedPlan:
             if self.all_ranks:
                 dist.all_reduce(fine, op=dist.ReduceOp.SUM, group=self.group)
             else:
-                dist.reduce(fine, dst=self.root, op=dist.ReduceOp.SUM, group=self.group)
+                dist.reduce(fine, dst=self.root_global, op=dist.ReduceOp.SUM, group=self.group)
                 if self.rank != self.root:
                     return None
             out = self.ops.new_modes() if out is None else out
             return self.ops.fft_deconvolve(fine, out)
         if not self.all_ranks:
-            dist.broadcast(inp, src=self.root, group=self.group)
+            dist.broadcast(inp, src=self.root_global, group=self.group)
         if hasattr(self.ops, "execute_type2"):
             if out is None:
                 out = self.ops.new_values(self.ops.plan.num_points)
@@ -139,5 +144,6 @@ class ReplicaPlan:
         return self.plan.execute(inp, out)
 
     def reduce_result(self, t):
-        dist.reduce(t, dst=self.root, op=dist.ReduceOp.SUM, group=self.group)
+        dst = self.root if self.group is None else dist.get_global_rank(self.group, self.root)
+        dist.reduce(t, dst=dst, op=dist.ReduceOp.SUM, group=self.group)
         return t

@@ -107,19 +107,13 @@ def centered_freqs(n):
 
 def build_correction_factors(grid, params):
     """kernel.py:181-205: (2/w)^d prod_i phi_hat(alpha_i k_i)^-1 over the
-    centered mode grid, shaped (N_d, ..., N_1), in the plan's real dtype."""
+    centered mode grid, shaped (N_d, ..., N_1), in the plan's real dtype.
+    Computed by the C library (nk_correction_factors, csrc/nk_host.cpp)."""
     d = grid.dim
-    floor = np.finfo(params.real_dtype).tiny * 100
-    axis_ft = []
-    for i in range(d):
-        xi = params.alpha[i] * centered_freqs(grid.modes[i])
-        ft = np.atleast_1d(kernel_fourier(params.beta, xi))
-        if np.any(ft <= floor):
-            raise ValueError("kernel Fourier transform underflowed on axis "
-                             f"{i + 1}; correction factors would overflow")
-        axis_ft.append(ft)
-    prod = axis_ft[-1]
-    for ft in axis_ft[-2::-1]:
-        prod = np.multiply.outer(prod, ft)
-    values = (2.0 / params.w) ** d / prod
-    return values.astype(params.real_dtype)
+    modes = (ctypes.c_int64 * d)(*[int(m) for m in grid.modes])
+    alpha = (ctypes.c_double * d)(*[float(a) for a in params.alpha])
+    out = np.empty(tuple(int(m) for m in grid.modes[::-1]), dtype=params.real_dtype)
+    rc = _lib.lib().nk_correction_factors(float(params.beta), int(params.w), d, modes, alpha,
+                                          _lib.PRECISIONS[params.precision], out.ctypes.data)
+    _lib.check(rc)
+    return out

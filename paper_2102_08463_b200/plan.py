@@ -86,14 +86,17 @@ class TransformPlan:
         nufft_type: 1 (nonuniform -> uniform) or 2 (uniform -> nonuniform).
         modes: (N_1, N_2[, N_3]) mode counts, axis 1 first.
         epsilon: tolerance in (0, 1).
-        method: "gm", "gmsort", "sm" or "default" (SM for type 1, GM-sort for
-            type 2).  For type 2 "sm" selects the shared-memory
-            staged gather (an extension; same per-point arithmetic).
+        method: "gm", "gmsort", "sm" or "default".  "default" is SM for both
+            types: type 1 as SPEC.md:170; for type 2 SPEC.md:170 names
+            GM-sort, and this library deviates on purpose -- "sm" there is the
+            shared-memory staged gather (same per-point arithmetic, measured
+            1.4-2.5x faster than GM-sort on B200).
         precision: "single" or "double".
         workers: accepted for API compatibility with the CPU reference
             (SPEC.md:176); the GPU grid replaces the worker pool.
-        bin_dims, max_subproblem: bin edge lengths (axis 1 first) and M_sub
-            (binsort.py:34-38 defaults).
+        bin_dims, max_subproblem: bin edge lengths (axis 1 first) and M_sub.
+            Unset: GM-sort plans keep the reference defaults (binsort.py:34-38);
+            SM plans use B200-tuned shapes (include/nufft_b200.h nk_opts).
         fine: explicit fine-grid sizes (default: the SPEC sizing rule).
         device: CUDA device (default: current).
         timing: record per-stage CUDA events (see stage_times()).

@@ -470,7 +470,7 @@ def test_two_stage_start_order_fallback(nk, orc):
     256^3 unit bins: 24 + 10 bits) setpts falls back to two stable sorts
     (start, then bin); results must match the GM-sort plan and the exported
     layout must stay the reference's bin-stable one."""
-    modes, eps, M = (128, 128, 128), 1e-5, 20000
+    modes, eps, M = (128, 128, 128), 1e-5, 20001   # odd M: scratch alignment
     grid = orc.make_grid(modes, eps, "single")
     pts = orc.gen_points("rand", M, grid, 9, np.float32)
     c = orc.gen_strengths(M, 9).astype(np.complex64)

@@ -308,6 +308,16 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     p->max_pad_cells = 1;
     for (int i = 0; i < dim; ++i) p->max_pad_cells *= p->bin_dims[i] + 2 * p->halo;
     p->method = method;
+    // footprint-start code space (setpts K4d): lexicographic in the padded
+    // bin, or tile-major for the tiled f64 spread
+    const bool tiled = nk_spread_tiled(type, dim, precision, w, method);
+    const int tlg = tiled ? nk_tile_lg(w) : 0;
+    p->start_space = p->max_pad_cells;
+    if (tiled) {
+        p->start_space = (int64_t)1 << (3 * tlg);
+        for (int i = 0; i < dim; ++i)
+            p->start_space *= (p->bin_dims[i] + 2 * p->halo + (1 << tlg) - 1) >> tlg;
+    }
 
     // geometry for kernels
     Geom &g = p->geom;
@@ -321,6 +331,8 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     }
     g.halo = p->halo;
     g.w = w;
+    g.tiled = tiled ? 1 : 0;
+    g.tile_lg = tlg;
     g.beta = beta;
     g.betaf = (float)beta;
     g.betaf_log2e = (float)(beta * 1.4426950408889634);

@@ -100,6 +100,29 @@ __device__ __forceinline__ int nk_kernel_row(T u, const Geom &g, T *ker) {
     return (int)st;
 }
 
+// Double-precision kernel row from the degree-14 interior pieces
+// (EsPoly64, nk_es_poly.h: max abs error 6e-15 against the exact kernel)
+// and the exact exp/sqrt path for the two edge pieces.  Same contract as
+// nk_kernel_row: returns the local start cell ceil(u - w/2).
+template <int W>
+__device__ __forceinline__ int nk_kernel_row_poly(double u, const Geom &g, double *ker) {
+    const double st = ceil(u - 0.5 * W);
+    const double d = st - u;
+    const double z0 = d * (2.0 / W);
+    ker[0] = nk_es(z0, g);
+    ker[W - 1] = nk_es(z0 + (2.0 * (W - 1) / W), g);
+    const double s = fma(2.0, d, (double)(W - 1));
+    typedef EsPoly64<W> P;
+#pragma unroll
+    for (int r = 1; r < W - 1; ++r) {
+        double p = P::c(r - 1, P::D);
+#pragma unroll
+        for (int k = P::D - 1; k >= 0; --k) p = fma(p, s, P::c(r - 1, k));
+        ker[r] = p;
+    }
+    return (int)st;
+}
+
 // Packed FMA with a broadcast constant addend: (a.x, a.y) * (b.x, b.y) + (c, c)
 // (sm_100 FFMA2 with a 32-bit immediate when c is a compile-time constant).
 __device__ __forceinline__ float2 nk_fma2_cc(float2 a, float2 b, float c) {
@@ -169,6 +192,20 @@ __device__ __forceinline__ void nk_red(float2 *p, float re, float im) {
 __device__ __forceinline__ void nk_red(double2 *p, double re, double im) {
     atomicAdd(&p->x, re);
     atomicAdd(&p->y, im);
+}
+
+// Footprint-start visit code of a point in its bin's padded frame (setpts
+// K4d sorts by bin, then this code): lexicographic (t3 p2 + t2) p1 + t1, or
+// for tiled plans tile-major -- all starts of one 2^L x 2^L x 2^L tile are
+// adjacent, so the tiled f64 spread (K6t) accumulates them in one register
+// window.
+__device__ __forceinline__ int nk_start_code(int t1, int t2, int t3, int p1, int p2,
+                                             const Geom &g) {
+    if (!g.tiled) return (t3 * p2 + t2) * p1 + t1;
+    const int L = g.tile_lg, m = (1 << L) - 1;
+    const int nt1 = (p1 + m) >> L, nt2 = (p2 + m) >> L;
+    const int tile = ((t3 >> L) * nt2 + (t2 >> L)) * nt1 + (t1 >> L);
+    return (tile << (3 * L)) | ((((t3 & m) << L) | (t2 & m)) << L) | (t1 & m);
 }
 
 // Decode a bin key into its corner cells (axis 1 fastest, binsort.py:103-111).

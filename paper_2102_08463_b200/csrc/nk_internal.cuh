@@ -39,6 +39,11 @@ struct Geom {
     int nb[3];      // bins per axis
     int halo;       // ceil(w/2)
     int w;
+    // footprint-start visit code (setpts K4d): 0 = lexicographic
+    // (t3 p2 + t2) p1 + t1; else tiles of 2^tile_lg starts per axis, tile
+    // major (the tiled f64 spread, nk_spread.cu K6t, groups a tile's points)
+    int tile_lg;
+    int tiled;
     double scale[3];  // n_i / (2 pi), binsort.py:99
     float betaf, betaf_log2e;
     double beta;
@@ -116,6 +121,7 @@ struct nk_plan {
     int32_t *d_sub_bin, *d_sub_start, *d_sub_stop;
     int max_sub_smem;       // bytes of dynamic smem for the SM kernels
     int64_t max_pad_cells;  // prod(m_i + 2 halo)
+    int64_t start_space;    // footprint-start codes per bin (nk_start_code range)
 
     // staging for host pointers
     void *d_in_stage, *d_out_stage;
@@ -142,6 +148,18 @@ struct nk_plan {
 // vs 1.37 with 4, 2.10 with 8, 1.61 with 1); above, NW = w: every warp owns
 // exactly one plane of every footprint.
 constexpr int nk_sm3_warps(int w) { return w <= 8 ? 2 : w; }
+// Tiled f64 3D spread (K6t, nk_spread.cu): 3D double type 1 SM plans with
+// 9 <= w <= 16.  A CTA of 16 warps holds a 16 x 16 x 16 register window
+// (warp = plane, lane = 16 x-cells x 8 rows); all points whose footprint
+// starts fall in one tile of 2^L x 2^L x 2^L start values share it, with
+// 2^L the largest power of two such that w + 2^L - 1 <= 16.
+constexpr int kTileWin = 16;
+constexpr int kTileBatch = 64;   // points staged per batch
+constexpr int nk_tile_lg(int w) { return w + 7 <= kTileWin ? 3 : (w + 3 <= kTileWin ? 2 : (w + 1 <= kTileWin ? 1 : 0)); }
+inline bool nk_spread_tiled(int type, int dim, int prec, int w, int method) {
+    return type == 1 && dim == 3 && prec == NK_DOUBLE && w >= 9 && w <= 16 && method == NK_SM &&
+           !getenv("NK_SPREAD_NO_TILE");
+}
 // Points staged per batch by the plane-owned 3D SM spread (nk_spread.cu):
 // 64 keeps the staging small enough for more resident CTAs (C3a spread
 // 1.24 -> 1.08 ms vs 128).
@@ -156,7 +174,10 @@ inline int64_t nk_sm_smem_bytes(int type, int dim, int prec, int w, const int *b
     int64_t b = (cells * 2 * rs + 15) / 16 * 16;
     // staging per point: int4 start, k1 row (double: zero-padded to 32),
     // k2 row, c * k3 row (complex)
-    if (type == 1 && dim == 3)
+    if (nk_spread_tiled(type, dim, prec, w, NK_SM))
+        // per point: int4 info, k1 / k2 window rows, c k3 window row (complex)
+        b += (int64_t)kTileBatch * (16 + 2 * kTileWin * rs + 2 * kTileWin * rs);
+    else if (type == 1 && dim == 3)
         b += (int64_t)nk_sm3_batch(prec) *
              (((prec == NK_DOUBLE && w <= 16) ? 32 : w) * rs + 3 * w * rs + 16);
     if (type == 1 && dim == 2) b += 128 + (32 * w * rs + 15) / 16 * 16 + 32 * w * 2 * rs;

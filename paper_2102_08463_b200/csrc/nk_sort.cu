@@ -73,7 +73,7 @@ k_fold_keys(int M, const TC *__restrict__ x, const TC *__restrict__ y,
     keys[i] = key;
     if (ckeys)
         ckeys[i] = (int32_t)(((unsigned)key << sb) |
-                             (unsigned)((t[2] * pd[1] + t[1]) * pd[0] + t[0]));
+                             (unsigned)nk_start_code(t[0], t[1], t[2], pd[0], pd[1], g));
     if (counts) {
         unsigned peers = __match_any_sync(mask, key);
         if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&counts[key], __popc(peers));
@@ -479,7 +479,7 @@ k_start_keys(int M, const int32_t *__restrict__ bin_keys, const T *__restrict__ 
     const int t1 = (int)nk_ceil<T>(pts[j] - half) + h;
     const int t2 = (int)nk_ceil<T>(pts[pitch + j] - half) + h;
     const int t3 = g.dim == 3 ? (int)nk_ceil<T>(pts[2 * pitch + j] - half) + h : 0;
-    skeys[j] = (t3 * p2 + t2) * p1 + t1;
+    skeys[j] = nk_start_code(t1, t2, t3, p1, p2, g);
 }
 
 __global__ void k_gather_i32(int M, const int32_t *__restrict__ idx,
@@ -639,7 +639,7 @@ static int order_by_start(nk_plan *p) {
     else
         k_start_keys<float><<<nb, 256, 0, st>>>((int)M, p->d_keys, (const float *)p->d_pts,
                                                 p->cap_M, p->geom, k0);
-    int rc = radix_sort_pairs(p, k0, nullptr, M, bits_for(p->max_pad_cells), p->d_alt_keys,
+    int rc = radix_sort_pairs(p, k0, nullptr, M, bits_for(p->start_space), p->d_alt_keys,
                               p->d_alt_vals, k1, v1);
     if (!rc) {
         k_gather_i32<<<nb, 256, 0, st>>>((int)M, p->d_alt_vals, p->d_keys, k0);
@@ -673,7 +673,7 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
     // sort of the composite key bin << sb | start (K1 computes both).  The
     // exported bin-stable perm is then derived on demand
     // (nk_compute_bin_perm).
-    const int sb = bits_for(p->max_pad_cells);
+    const int sb = bits_for(p->start_space);
     const bool composite = sort && p->method == NK_SM && sb + bits_for(nbins) <= 32;
     int32_t *ck = composite ? p->d_sort_scr : nullptr;
     NK_CUDA(cudaMemsetAsync(p->d_counts, 0, sizeof(int32_t) * nbins, st));

@@ -286,6 +286,194 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     }
 }
 
+// K6t: tiled f64 3D spread (w >= 9; C4 / C5).  The padded bin sits in
+// shared memory as in K6c; the CTA's 16 warps hold a 16 x 16 x 16-cell
+// register window of it: warp = window plane (absolute plane z == warp mod
+// 16, so warps own disjoint planes and read-modify-write shared memory
+// without atomics), lane = x cell (lane & 15) x 8 rows (lane >> 4 picks the
+// row half).  setpts orders each bin's points tile-major (nk_start_code):
+// every point whose footprint start lies in one tile of 2^L start values per
+// axis (w + 2^L - 1 <= 16) fits the window anchored at the tile corner, so
+// the group of all of them (C4 density: ~12 points) accumulates in registers
+// and writes shared memory once.  Per point a lane does 2 DMUL (c k3[e]
+// k1[x]) and 16 DFMA against 8 k2 values read as four 16-byte broadcasts;
+// kernel rows are staged pre-shifted into the window frame (zeros outside
+// the footprint), one (point, axis, window cell) value per thread.  Warps
+// whose plane is outside a point's footprint skip it.  Flush = native f64
+// reductions, one padded-bin row per warp pass (Eq. 17).
+template <int W>
+__global__ void __launch_bounds__(512, 1)
+k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
+               const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
+               const double *__restrict__ pts, int64_t pitch, const double2 *__restrict__ c,
+               Geom g, double2 *__restrict__ fine, int64_t stage_off) {
+    constexpr int WIN = kTileWin, NB = kTileBatch, L = nk_tile_lg(W), TM = (1 << L) - 1;
+    static_assert(W + TM <= WIN, "window too small for the tile");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2 *buf = reinterpret_cast<double2 *>(smem_raw);
+    int4 *sinfo = reinterpret_cast<int4 *>(smem_raw + stage_off);   // group, A1|A2|A3, sh3
+    double *sk1 = reinterpret_cast<double *>(sinfo + NB);            // [NB][16]
+    double *sk2 = sk1 + NB * WIN;                                    // [NB][16]
+    double2 *sck3 = reinterpret_cast<double2 *>(sk2 + NB * WIN);     // [NB][16]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int x = lane & (WIN - 1), rh = (lane >> 4) * 8;
+    const int s = blockIdx.x;
+    c += blockIdx.y * g.M;
+    fine += blockIdx.y * g.ntot;
+    int corner[3];
+    nk_bin_corner(sub_bin[s], g, corner);
+    const int h = g.halo;
+    const int p1 = min(g.m[0], g.n[0] - corner[0]) + 2 * h;
+    const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
+    const int p3 = min(g.m[2], g.n[2] - corner[2]) + 2 * h;
+    const int P = p1 * p2 * p3, pstride = p1 * p2;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) buf[i] = make_double2(0.0, 0.0);
+    const double half = 0.5 * W;
+    const int j0 = sub_start[s], j1 = sub_stop[s];
+    // stage window rows of points [b, b + nb): one thread per (point, axis)
+    // evaluates the kernel row (interior pieces as degree-14 polynomials,
+    // EsPoly64) and writes it shifted into the window frame, entry i =
+    // k[i - sh] (zeros outside the footprint; c folded into axis 3); the
+    // axis-1 thread also records the point's tile
+    auto stage = [&](int b, int nb) {
+        __syncthreads();   // previous batch consumed (and the bin zeroed)
+        for (int v = threadIdx.x; v < nb * 3; v += blockDim.x) {
+            const int q = v / 3, ax = v - 3 * q;
+            const int j = b + q;
+            double k[W];
+            const int t = nk_kernel_row_poly<W>(pts[ax * pitch + j], g, k) + h;
+            const int sh = t & TM;
+            if (ax == 2) {
+                const double2 cv = c[perm[j]];
+                double2 *dst = sck3 + q * WIN;
+#pragma unroll
+                for (int i = 0; i < WIN - W; ++i)
+                    dst[i < sh ? i : i + W] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int r = 0; r < W; ++r) dst[sh + r] = make_double2(cv.x * k[r], cv.y * k[r]);
+            } else {
+                double *dst = (ax == 0 ? sk1 : sk2) + q * WIN;
+#pragma unroll
+                for (int i = 0; i < WIN - W; ++i) dst[i < sh ? i : i + W] = 0.0;
+#pragma unroll
+                for (int r = 0; r < W; ++r) dst[sh + r] = k[r];
+            }
+            if (ax == 0) {
+                const double u2 = pts[pitch + j], u3 = pts[2 * pitch + j];
+                const int t2 = (int)ceil(u2 - half) + h, t3 = (int)ceil(u3 - half) + h;
+                sinfo[q] = make_int4(nk_start_code(t, t2, t3, p1, p2, g) >> (3 * L),
+                                     (t & ~TM) | ((t2 & ~TM) << 8) | ((t3 & ~TM) << 16),
+                                     t3 & TM, 0);
+            }
+        }
+        __syncthreads();
+    };
+    int base = j0, nb = min(NB, j1 - j0), q = 0;
+    if (nb > 0) stage(base, nb);
+    // one register window per tile group (CTA-uniform control flow)
+    while (q < nb) {
+        const int4 g0 = sinfo[q];
+        const int grp = g0.x;
+        const int a1 = g0.y & 0xff, a2 = (g0.y >> 8) & 0xff, a3 = g0.y >> 16;
+        const int e = (warp - a3) & (WIN - 1);   // the warp's window plane
+        double2 acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = make_double2(0.0, 0.0);
+        for (;;) {
+            if (q == nb) {   // next batch
+                base += nb;
+                nb = min(NB, j1 - base);
+                q = 0;
+                if (nb <= 0) break;
+                stage(base, nb);
+            }
+            if (sinfo[q].x != grp) break;
+            // the group's points in this batch, two-deep register pipeline:
+            // point q + 1's operands load while point q's DFMAs issue
+            struct Ops {
+                double2 ck, b0, b1, b2, b3;
+                double k1;
+            };
+            auto load = [&](int qq, Ops &o) {
+                o.ck = sck3[qq * WIN + e];
+                o.k1 = sk1[qq * WIN + x];
+                const double2 *k2p = reinterpret_cast<const double2 *>(sk2 + qq * WIN + rh);
+                o.b0 = k2p[0];
+                o.b1 = k2p[1];
+                o.b2 = k2p[2];
+                o.b3 = k2p[3];
+            };
+            auto fma8 = [&](const Ops &o) {
+                const double ar = o.ck.x * o.k1, ai = o.ck.y * o.k1;
+                const double kb[8] = {o.b0.x, o.b0.y, o.b1.x, o.b1.y,
+                                      o.b2.x, o.b2.y, o.b3.x, o.b3.y};
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    acc[i].x = fma(ar, kb[i], acc[i].x);
+                    acc[i].y = fma(ai, kb[i], acc[i].y);
+                }
+            };
+            Ops A, B;
+            int sh3 = sinfo[q].z;
+            load(q, A);
+            for (;;) {
+                int qn = q + 1;
+                int4 nx = qn < nb ? sinfo[qn] : make_int4(-1, 0, 0, 0);
+                load(min(qn, nb - 1), B);
+                if ((unsigned)(e - sh3) < (unsigned)W) fma8(A);   // warp-uniform
+                q = qn;
+                if (nx.x != grp) break;
+                sh3 = nx.z;
+                qn = q + 1;
+                nx = qn < nb ? sinfo[qn] : make_int4(-1, 0, 0, 0);
+                load(min(qn, nb - 1), A);
+                if ((unsigned)(e - sh3) < (unsigned)W) fma8(B);
+                q = qn;
+                if (nx.x != grp) break;
+                sh3 = nx.z;
+            }
+        }
+        // flush the warp's plane of the window; cells outside the padded bin
+        // carry zero sums (footprints lie inside)
+        const int zpl = a3 + e, xx = a1 + x;
+        if (zpl < p3 && xx < p1) {
+            double2 *col = buf + zpl * pstride + (a2 + rh) * p1 + xx;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (a2 + rh + i < p2) {
+                    double2 v = col[i * p1];
+                    v.x += acc[i].x;
+                    v.y += acc[i].y;
+                    col[i * p1] = v;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // merge with periodic wrap (Eq. 17): rows over warps, x over lanes
+    const int o1 = corner[0] - h, o2 = corner[1] - h, o3 = corner[2] - h;
+    constexpr int NWARP = 16;
+    int zz = 0, yy = warp;   // row r = zz p2 + yy, r = warp, warp + 16, ...
+    while (yy >= p2) {
+        yy -= p2;
+        ++zz;
+    }
+    for (; zz < p3;) {
+        double2 *row = fine + ((int64_t)nk_wrap(o3 + zz, g.n[2]) * g.n[1] +
+                               nk_wrap(o2 + yy, g.n[1])) * (int64_t)g.n[0];
+        const double2 *src = buf + (zz * p2 + yy) * p1;
+        for (int xx = lane; xx < p1; xx += 32) {
+            const double2 v = src[xx];
+            if (v.x != 0.0 || v.y != 0.0) nk_red(row + nk_wrap(o1 + xx, g.n[0]), v.x, v.y);
+        }
+        yy += NWARP;
+        while (yy >= p2) {
+            yy -= p2;
+            ++zz;
+        }
+    }
+}
+
 // K6c-2D: one warp per subproblem.  The warp owns the whole padded bin, so
 // its lanes can cover one point's w x w footprint with plain shared-memory
 // read-modify-writes (distinct cells per pass, points in sequence): no
@@ -406,6 +594,22 @@ int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
     typedef typename cplx<T>::t C;
     const int M = (int)p->M;
     if (M == 0) return NK_OK;
+    if constexpr (D == 3 && sizeof(T) == 8 && W >= 9) {
+        if (p->method == NK_SM && p->geom.tiled) {
+            if (p->S == 0) return NK_OK;
+            size_t smem = (size_t)p->max_sub_smem;
+            auto kern = k_spread_tiled<W>;
+            NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+            int64_t stage_off = (p->max_pad_cells * (int64_t)sizeof(C) + 15) / 16 * 16;
+            kern<<<dim3((unsigned)p->S, p->ntrans), 512, smem, p->stream>>>(
+                p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm, (const double *)p->d_pts,
+                p->cap_M, (const double2 *)c, p->geom, (double2 *)fine, stage_off);
+            NK_LAUNCH_CHECK();
+            ++*launches;
+            return NK_OK;
+        }
+    }
     if (p->method == NK_SM && D == 3) {
         if (p->S == 0) return NK_OK;
         size_t smem = (size_t)p->max_sub_smem;

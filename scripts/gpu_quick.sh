@@ -9,5 +9,5 @@ fi
 for item in $CFGS; do
   name=${item%%:*}; args=${item#*:}; args=${args//,/ }
   timeout 900 python bench.py --no-cpu-baseline $args > gpurun_out/q/$name.json 2> gpurun_out/q/$name.err
-  echo "$name: $(python -c "import json,sys; d=json.load(open('gpurun_out/q/$name.json')); print('%.3e'%d['value'], 'ms', round(d['ms_per_step'],4), {k:round(v,4) for k,v in d.get('stage_ms',{}).items()}, d['config'].get('bin_dims'))" 2>&1 | tail -1)"
+  echo "$name: $(python -c "import json,sys; d=json.load(open('gpurun_out/q/$name.json')); print('%.3e'%d['value'], 'ms', round(d['ms_per_step'],4), d.get('stage_ms'), d['config'].get('bin_dims'))" 2>&1 | tail -1)"
 done

@@ -511,6 +511,36 @@ def test_xwin_interp_matches_per_thread_gather(nk, orc, dist, eps, monkeypatch):
     assert orc.rel_l2_error(got, orc.direct_type2(pts, f, modes)) < 10 * eps
 
 
+@pytest.mark.parametrize("dist,eps,bins", [("rand", 1e-12, None), ("cluster", 1e-9, None),
+                                           ("rand", 1e-11, (5, 3, 7)), ("gauss", 1e-15, None),
+                                           ("rand", 1e-8, (6, 6, 2))])
+def test_tiled_spread_matches_plane_spread(nk, orc, dist, eps, bins, monkeypatch):
+    """3D double type 1 with w >= 9 spreads through tile-group register
+    windows (K6t: setpts orders each bin tile-major, a CTA of 16 plane warps
+    accumulates every point of a start tile in registers).  Must match the
+    plane-owned x-window spread (K6c, NK_SPREAD_NO_TILE=1) to rounding -- with
+    odd user bins (partial tiles, edge bins), clustered points and w = 9 / 16
+    (tile 8 / 1) -- and direct sums (10 eps)."""
+    modes, M = (24, 20, 16), 7001
+    grid = orc.make_grid(modes, eps, "double")
+    pts = orc.gen_points(dist, M, grid, 33, np.float64)
+    c = orc.gen_strengths(M, 3)
+    kw = {} if bins is None else {"bin_dims": bins}
+    p = nk.make_plan(1, modes, eps, "sm", "double", **kw)
+    p.set_points(pts)
+    got = p.execute(c)
+    monkeypatch.setenv("NK_SPREAD_NO_TILE", "1")
+    q = nk.make_plan(1, modes, eps, "sm", "double", **kw)
+    q.set_points(pts)
+    ref = q.execute(c)
+    assert orc.rel_l2_error(got, ref) < 1e-14
+    # the exported layout stays the reference's bin-stable one
+    keys, counts, starts, perm = (t.cpu().numpy() for t in p.layout_tensors())
+    lay = orc.bin_sort(pts, orc.GridSpec(modes, p.grid.fine), p.bin_dims)
+    assert np.array_equal(perm, lay.perm) and np.array_equal(starts, lay.starts)
+    assert orc.rel_l2_error(got, orc.direct_type1(pts, c, modes)) < max(10 * eps, 1e-13)
+
+
 @pytest.mark.parametrize("modes", [(128, 96), (512, 300), (1024, 40)])
 def test_fused_pad_rowfft_type2(nk, orc, modes, monkeypatch):
     """2D single-precision type 2 with n_1 = 2^L runs K9 fused with the row

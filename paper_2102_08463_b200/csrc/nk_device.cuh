@@ -123,6 +123,58 @@ __device__ __forceinline__ int nk_kernel_row_poly(double u, const Geom &g, doubl
     return (int)st;
 }
 
+// FP64 tensor-core MMA (DMMA.8x8x4): C[8x8] += A[8x4] B[4x8], row-major A,
+// column-major B.  Lane l holds A[l / 4][l % 4], B[l % 4][l / 4] and
+// C[l / 4][2 (l % 4) + {0, 1}].  B200 runs it at the FP64 peak (63 FMA / clk /
+// SM measured, scripts/dmma_peak.cu) for 1/8 of the issue slots of DFMA.
+__device__ __forceinline__ void nk_dmma(double &c0, double &c1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// ---- TMA bulk copies + mbarriers (sm_90+/sm_100 async proxy) ----------
+__device__ __forceinline__ uint32_t nk_smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void nk_mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(nk_smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+// make the initialised barriers visible to the async (TMA) proxy
+__device__ __forceinline__ void nk_fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// order this thread's earlier generic-proxy shared accesses (made visible to
+// it by a barrier) before its subsequent async-proxy (TMA) writes
+__device__ __forceinline__ void nk_fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void nk_mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(nk_smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+// 1D TMA bulk copy global -> shared (16-byte aligned, size a multiple of 16),
+// completion counted in bytes on the mbarrier (UBLKCP)
+__device__ __forceinline__ void nk_bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            nk_smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(nk_smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void nk_mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "NK_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra NK_WAIT_%=;\n\t}" ::"r"(nk_smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 // Packed FMA with a broadcast constant addend: (a.x, a.y) * (b.x, b.y) + (c, c)
 // (sm_100 FFMA2 with a 32-bit immediate when c is a compile-time constant).
 __device__ __forceinline__ float2 nk_fma2_cc(float2 a, float2 b, float c) {

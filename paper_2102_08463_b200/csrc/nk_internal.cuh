@@ -90,6 +90,8 @@ struct nk_plan {
     bool fft_col_ok;
     void *d_twiddle;        // n_1 complex exp(+2 pi i k / n_1)
     int *d_work;            // n_trans work counters of the staged interpolation
+    void *d_cvis;           // strengths gathered into visit order (tiled f64 spread)
+    int64_t cap_cvis;
 
     // points
     int64_t M;
@@ -154,7 +156,10 @@ constexpr int nk_sm3_warps(int w) { return w <= 8 ? 2 : w; }
 // starts fall in one tile of 2^L x 2^L x 2^L start values share it, with
 // 2^L the largest power of two such that w + 2^L - 1 <= 16.
 constexpr int kTileWin = 16;
-constexpr int kTileBatch = 64;   // points staged per batch
+#ifndef NK_TILE_NB
+#define NK_TILE_NB 32
+#endif
+constexpr int kTileBatch = NK_TILE_NB;   // points per staged batch (two buffers)
 constexpr int nk_tile_lg(int w) { return w + 7 <= kTileWin ? 3 : (w + 3 <= kTileWin ? 2 : (w + 1 <= kTileWin ? 1 : 0)); }
 inline bool nk_spread_tiled(int type, int dim, int prec, int w, int method) {
     return type == 1 && dim == 3 && prec == NK_DOUBLE && w >= 9 && w <= 16 && method == NK_SM &&
@@ -176,7 +181,9 @@ inline int64_t nk_sm_smem_bytes(int type, int dim, int prec, int w, const int *b
     // k2 row, c * k3 row (complex)
     if (nk_spread_tiled(type, dim, prec, w, NK_SM))
         // per point: int4 info, k1 / k2 window rows, c k3 window row (complex)
-        b += (int64_t)kTileBatch * (16 + 2 * kTileWin * rs + 2 * kTileWin * rs);
+        b += 2 * ((int64_t)kTileBatch * (16 + 2 * kTileWin * rs + 2 * kTileWin * rs) +
+                  2 * kTileWin * 4 * rs) +
+             3 * (3 * (kTileBatch + 2) * rs + kTileBatch * 2 * rs) + 32;   // + TMA ring
     else if (type == 1 && dim == 3)
         b += (int64_t)nk_sm3_batch(prec) *
              (((prec == NK_DOUBLE && w <= 16) ? 32 : w) * rs + 3 * w * rs + 16);

@@ -286,39 +286,66 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     }
 }
 
-// K6t: tiled f64 3D spread (w >= 9; C4 / C5).  The padded bin sits in
-// shared memory as in K6c; the CTA's 16 warps hold a 16 x 16 x 16-cell
-// register window of it: warp = window plane (absolute plane z == warp mod
-// 16, so warps own disjoint planes and read-modify-write shared memory
-// without atomics), lane = x cell (lane & 15) x 8 rows (lane >> 4 picks the
-// row half).  setpts orders each bin's points tile-major (nk_start_code):
-// every point whose footprint start lies in one tile of 2^L start values per
-// axis (w + 2^L - 1 <= 16) fits the window anchored at the tile corner, so
-// the group of all of them (C4 density: ~12 points) accumulates in registers
-// and writes shared memory once.  Per point a lane does 2 DMUL (c k3[e]
-// k1[x]) and 16 DFMA against 8 k2 values read as four 16-byte broadcasts;
-// kernel rows are staged pre-shifted into the window frame (zeros outside
-// the footprint), one (point, axis, window cell) value per thread.  Warps
-// whose plane is outside a point's footprint skip it.  Flush = native f64
-// reductions, one padded-bin row per warp pass (Eq. 17).
+// Strengths in visit order for the tiled spread: cv[t][j] = c[t][perm[j]]
+// (one pass per execute; the spread then streams contiguous slices by TMA).
+__global__ void __launch_bounds__(256)
+k_gather_visit(int M, const int32_t *__restrict__ perm, const double2 *__restrict__ c,
+               int64_t cpitch, double2 *__restrict__ cv, int64_t vpitch) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < M) cv[blockIdx.y * vpitch + j] = c[blockIdx.y * cpitch + perm[j]];
+}
+inline int64_t g_M(const nk_plan *p) { return p->M; }
+
+// K6t: tiled f64 3D spread on the FP64 tensor cores (w >= 9; C4 / C5).
+// The padded bin sits in shared memory as in K6c.  setpts orders each bin's
+// points tile-major (nk_start_code): every point whose footprint start lies
+// in one tile of 2^L start values per axis (w + 2^L - 1 <= 16) fits the
+// 16 x 16 x 16-cell window anchored at the tile corner, and the group of
+// all of them (C4 density: ~12 points) is spread as one small GEMM per
+// window plane: warp = plane (absolute plane z == warp mod 16, so warps own
+// disjoint planes and read-modify-write shared memory without atomics),
+//   C[x][(y, re|im)] += sum_p k1_p[x] * (k2_p[y] (c k3_p[z]))_{re|im},
+// 2 x-tiles x 4 y-tiles of DMMA m8n8k4 (K = 4 points per step) -- 1/8 of
+// the issue slots of the equivalent DFMAs, at the same FP64 peak.  A lane's
+// accumulator pair is one complex cell (x, y), so the group's flush is 8
+// 16-byte read-modify-writes per lane.  Kernel rows are staged pre-shifted
+// into the window frame (zeros outside the footprint, so planes outside a
+// point's footprint contribute nothing and all-zero steps are skipped) by
+// one thread per (point, axis) with degree-14 polynomial pieces (EsPoly64),
+// double-buffered: batch b + 1 is staged between the barrier that retires
+// batch b - 1 and the DMMAs of batch b.  Flush = native f64 reductions, one
+// padded-bin row per warp pass (Eq. 17).
 template <int W>
 __global__ void __launch_bounds__(512, 1)
 k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
-               const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
-               const double *__restrict__ pts, int64_t pitch, const double2 *__restrict__ c,
-               Geom g, double2 *__restrict__ fine, int64_t stage_off) {
+               const int32_t *__restrict__ sub_stop, const double *__restrict__ pts,
+               int64_t pitch, const double2 *__restrict__ cvis, Geom g,
+               double2 *__restrict__ fine, int64_t stage_off, int dbg) {
     constexpr int WIN = kTileWin, NB = kTileBatch, L = nk_tile_lg(W), TM = (1 << L) - 1;
+    constexpr int NWARP = 16;
     static_assert(W + TM <= WIN, "window too small for the tile");
+    static_assert(NB <= 32, "one boundary mask word per batch");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2 *buf = reinterpret_cast<double2 *>(smem_raw);
-    int4 *sinfo = reinterpret_cast<int4 *>(smem_raw + stage_off);   // group, A1|A2|A3, sh3
-    double *sk1 = reinterpret_cast<double *>(sinfo + NB);            // [NB][16]
-    double *sk2 = sk1 + NB * WIN;                                    // [NB][16]
-    double2 *sck3 = reinterpret_cast<double2 *>(sk2 + NB * WIN);     // [NB][16]
+    // two staging buffers: info [NB], k1 rows [NB][16], k2 rows [NB][16],
+    // c k3 rows [NB][16] (complex)
+    unsigned char *stg = smem_raw + stage_off;
+    // rows stored transposed, [window cell][point]: a DMMA step's 4
+    // consecutive points are adjacent words; k rows are padded to NB + 4
+    // points so that 4 cells x 4 points of a half-warp hit distinct banks
+    constexpr int KS = NB + 4;
+    constexpr int SB = NB * 16 + 2 * WIN * KS * 8 + WIN * NB * 16;
+    auto sinfo_of = [&](int bi) { return reinterpret_cast<int4 *>(stg + bi * SB); };
+    auto sk1_of = [&](int bi) { return reinterpret_cast<double *>(stg + bi * SB + NB * 16); };
+    auto sk2_of = [&](int bi) { return sk1_of(bi) + WIN * KS; };
+    auto sck3_of = [&](int bi) { return reinterpret_cast<double2 *>(sk2_of(bi) + WIN * KS); };
+    // raw inputs ring (3 slots, TMA bulk copies): u_axis [NB + 2] x 3, c [NB]
+    constexpr int RU = NB + 2, RB = 3 * RU * 8 + NB * 16;
+    unsigned char *raw = stg + 2 * SB;
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(raw + 3 * RB);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int x = lane & (WIN - 1), rh = (lane >> 4) * 8;
     const int s = blockIdx.x;
-    c += blockIdx.y * g.M;
+    cvis += blockIdx.y * pitch;
     fine += blockIdx.y * g.ntot;
     int corner[3];
     nk_bin_corner(sub_bin[s], g, corner);
@@ -330,141 +357,229 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
     for (int i = threadIdx.x; i < P; i += blockDim.x) buf[i] = make_double2(0.0, 0.0);
     const double half = 0.5 * W;
     const int j0 = sub_start[s], j1 = sub_stop[s];
-    // stage window rows of points [b, b + nb): one thread per (point, axis)
-    // evaluates the kernel row (interior pieces as degree-14 polynomials,
-    // EsPoly64) and writes it shifted into the window frame, entry i =
-    // k[i - sh] (zeros outside the footprint; c folded into axis 3); the
-    // axis-1 thread also records the point's tile
-    auto stage = [&](int b, int nb) {
-        __syncthreads();   // previous batch consumed (and the bin zeroed)
-        for (int v = threadIdx.x; v < nb * 3; v += blockDim.x) {
+    // stage window rows of points [b, b + nb) into buffer bi: row v = (point
+    // q, axis) runs on lane v / 16 of warp v % 16 (every warp gets its share,
+    // no barrier); entry i = k[i - sh] (c folded into axis 3); the axis-1
+    // thread also records the point's tile
+    // TMA: batch k's coordinates and strengths into raw slot k % 3
+    auto issue = [&](int k) {
+        const int b = j0 + k * NB, nb = min(NB, j1 - b);
+        if (nb <= 0) return;
+        unsigned char *slot = raw + (k % 3) * RB;
+        const int b0 = b & ~1;                           // 16-byte aligned start
+        const unsigned ub = (unsigned)(((b + nb - b0) + 1) & ~1) * 8u;
+        nk_fence_proxy_async();
+        nk_mbar_expect_tx(mbar + k % 3, 3 * ub + 16u * nb);
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax)
+            nk_bulk_g2s(slot + ax * RU * 8, pts + ax * pitch + b0, ub, mbar + k % 3);
+        nk_bulk_g2s(slot + 3 * RU * 8, cvis + b, 16u * nb, mbar + k % 3);
+    };
+    auto stage = [&](int k, int bi) {
+        const int b = j0 + k * NB, nb = min(NB, j1 - b);
+        int4 *sinfo = sinfo_of(bi);
+        double *sk1 = sk1_of(bi), *sk2 = sk2_of(bi);
+        double2 *sck3 = sck3_of(bi);
+        const unsigned char *slot = raw + (k % 3) * RB;
+        const double *ru = reinterpret_cast<const double *>(slot) + (b - (b & ~1));
+        const double2 *rc = reinterpret_cast<const double2 *>(slot + 3 * RU * 8);
+        nk_mbar_wait(mbar + k % 3, (k / 3) & 1);
+        const int v = lane * NWARP + warp;
+        if (v < nb * 3) {
             const int q = v / 3, ax = v - 3 * q;
-            const int j = b + q;
             double k[W];
-            const int t = nk_kernel_row_poly<W>(pts[ax * pitch + j], g, k) + h;
+            int t;
+            if (dbg & 8) {
+                t = (int)ceil(ru[ax * RU + q] - half) + h;
+#pragma unroll
+                for (int r = 0; r < W; ++r) k[r] = 0.5;
+            } else {
+                t = nk_kernel_row_poly<W>(ru[ax * RU + q], g, k) + h;
+            }
             const int sh = t & TM;
             if (ax == 2) {
-                const double2 cv = c[perm[j]];
-                double2 *dst = sck3 + q * WIN;
+                const double2 cv = rc[q];
+                double2 *dst = sck3 + q;
 #pragma unroll
                 for (int i = 0; i < WIN - W; ++i)
-                    dst[i < sh ? i : i + W] = make_double2(0.0, 0.0);
+                    dst[(i < sh ? i : i + W) * NB] = make_double2(0.0, 0.0);
 #pragma unroll
-                for (int r = 0; r < W; ++r) dst[sh + r] = make_double2(cv.x * k[r], cv.y * k[r]);
+                for (int r = 0; r < W; ++r)
+                    dst[(sh + r) * NB] = make_double2(cv.x * k[r], cv.y * k[r]);
             } else {
-                double *dst = (ax == 0 ? sk1 : sk2) + q * WIN;
+                double *dst = (ax == 0 ? sk1 : sk2) + q;
 #pragma unroll
-                for (int i = 0; i < WIN - W; ++i) dst[i < sh ? i : i + W] = 0.0;
+                for (int i = 0; i < WIN - W; ++i) dst[(i < sh ? i : i + W) * KS] = 0.0;
 #pragma unroll
-                for (int r = 0; r < W; ++r) dst[sh + r] = k[r];
+                for (int r = 0; r < W; ++r) dst[(sh + r) * KS] = k[r];
             }
             if (ax == 0) {
-                const double u2 = pts[pitch + j], u3 = pts[2 * pitch + j];
+                const double u2 = ru[RU + q], u3 = ru[2 * RU + q];
                 const int t2 = (int)ceil(u2 - half) + h, t3 = (int)ceil(u3 - half) + h;
                 sinfo[q] = make_int4(nk_start_code(t, t2, t3, p1, p2, g) >> (3 * L),
                                      (t & ~TM) | ((t2 & ~TM) << 8) | ((t3 & ~TM) << 16),
                                      t3 & TM, 0);
             }
         }
-        __syncthreads();
     };
-    int base = j0, nb = min(NB, j1 - j0), q = 0;
-    if (nb > 0) stage(base, nb);
-    // one register window per tile group (CTA-uniform control flow)
-    while (q < nb) {
+    // batch state: batch kb = [j0 + kb NB, +nb) in staging buffer kb & 1;
+    // batch kb + 1 is staged, batch kb + 2's raw inputs are in flight
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) nk_mbar_init(mbar + i, 1);
+        nk_fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        issue(0);
+        issue(1);
+        issue(2);
+    }
+    int kb = 0;
+    int nb = min(NB, j1 - j0);
+    if (nb > 0) stage(0, 0);
+    __syncthreads();   // batch 0 staged, bin zeroed
+    if (j1 - j0 > NB) stage(1, 1);
+    const int4 *sinfo = sinfo_of(0);
+    const double *sk1 = sk1_of(0), *sk2 = sk2_of(0);
+    const double2 *sck3 = sck3_of(0);
+    // group boundaries of the current batch as a bit mask (bit q: point q
+    // starts a new group), so the chunk loop knows its segment [q, qe)
+    unsigned bnd = 0;
+    auto boundaries = [&]() {
+        const int ga = lane < nb ? sinfo[lane].x : -1;
+        const int pa = __shfl_up_sync(0xffffffffu, ga, 1);
+        bnd = __ballot_sync(0xffffffffu, lane < nb && (lane == 0 || ga != pa));
+    };
+    // retire the current batch, switch to the staged one, stage the next
+    auto advance = [&]() {
+        __syncthreads();   // every warp is done with batch kb; kb + 1 is staged
+        ++kb;
+        nb = min(NB, j1 - (j0 + kb * NB));
+        if (threadIdx.x == 0) issue(kb + 2);   // into the slot batch kb - 1 used
+        if (j1 - (j0 + (kb + 1) * NB) > 0) stage(kb + 1, (kb + 1) & 1);
+        sinfo = sinfo_of(kb & 1);
+        sk1 = sk1_of(kb & 1);
+        sk2 = sk2_of(kb & 1);
+        sck3 = sck3_of(kb & 1);
+        if (nb > 0) boundaries();
+    };
+    if (nb > 0) boundaries();
+    const int kp = lane & 3, row = lane >> 2, ycol = lane >> 3, cpart = (lane >> 2) & 1;
+    int q = 0;
+    while (nb > 0) {
+        if (q == nb) {
+            advance();
+            q = 0;
+            continue;
+        }
+        // a tile group (CTA-uniform control flow)
         const int4 g0 = sinfo[q];
         const int grp = g0.x;
         const int a1 = g0.y & 0xff, a2 = (g0.y >> 8) & 0xff, a3 = g0.y >> 16;
         const int e = (warp - a3) & (WIN - 1);   // the warp's window plane
-        double2 acc[8];
+        // lane (row lane / 4, column pair lane % 4) holds cell (x, y) as (re, im)
+        double acc[2][4][2];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = make_double2(0.0, 0.0);
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
         for (;;) {
-            if (q == nb) {   // next batch
-                base += nb;
-                nb = min(NB, j1 - base);
-                q = 0;
-                if (nb <= 0) break;
-                stage(base, nb);
-            }
-            if (sinfo[q].x != grp) break;
-            // the group's points in this batch, two-deep register pipeline:
-            // point q + 1's operands load while point q's DFMAs issue
+            // the group's segment of this batch: [q, qe)
+            const unsigned rest = q + 1 < 32 ? bnd >> (q + 1) : 0u;
+            const int qe = rest ? min(nb, q + __ffs(rest)) : nb;
+            // chunks of 4 points (lane k-index = point cq + kp); the next
+            // chunk's operands load while the current chunk's DMMAs issue
             struct Ops {
-                double2 ck, b0, b1, b2, b3;
-                double k1;
+                double2 ck;
+                double a0, a8, k2[4];
             };
-            auto load = [&](int qq, Ops &o) {
-                o.ck = sck3[qq * WIN + e];
-                o.k1 = sk1[qq * WIN + x];
-                const double2 *k2p = reinterpret_cast<const double2 *>(sk2 + qq * WIN + rh);
-                o.b0 = k2p[0];
-                o.b1 = k2p[1];
-                o.b2 = k2p[2];
-                o.b3 = k2p[3];
-            };
-            auto fma8 = [&](const Ops &o) {
-                const double ar = o.ck.x * o.k1, ai = o.ck.y * o.k1;
-                const double kb[8] = {o.b0.x, o.b0.y, o.b1.x, o.b1.y,
-                                      o.b2.x, o.b2.y, o.b3.x, o.b3.y};
+            auto load = [&](int cq, Ops &o) {
+                const int qp = min(cq + kp, qe - 1);
+                o.ck = sck3[e * NB + qp];
+                if (cq + kp >= qe) o.ck = make_double2(0.0, 0.0);
+                o.a0 = sk1[row * KS + qp];
+                o.a8 = sk1[(8 + row) * KS + qp];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    acc[i].x = fma(ar, kb[i], acc[i].x);
-                    acc[i].y = fma(ai, kb[i], acc[i].y);
+                for (int nt = 0; nt < 4; ++nt) o.k2[nt] = sk2[(nt * 4 + ycol) * KS + qp];
+            };
+            auto mma = [&](const Ops &o) {
+                // plane e outside every chunk point's footprint: c k3 = 0
+                if (!(dbg & 4) && __any_sync(0xffffffffu, o.ck.x != 0.0 || o.ck.y != 0.0)) {
+                    const double ckc = cpart ? o.ck.y : o.ck.x;
+#pragma unroll
+                    for (int nt = 0; nt < 4; ++nt) {
+                        const double bv = o.k2[nt] * ckc;
+                        nk_dmma(acc[0][nt][0], acc[0][nt][1], o.a0, bv);
+                        nk_dmma(acc[1][nt][0], acc[1][nt][1], o.a8, bv);
+                    }
                 }
             };
             Ops A, B;
-            int sh3 = sinfo[q].z;
             load(q, A);
+            int cq = q;
             for (;;) {
-                int qn = q + 1;
-                int4 nx = qn < nb ? sinfo[qn] : make_int4(-1, 0, 0, 0);
-                load(min(qn, nb - 1), B);
-                if ((unsigned)(e - sh3) < (unsigned)W) fma8(A);   // warp-uniform
-                q = qn;
-                if (nx.x != grp) break;
-                sh3 = nx.z;
-                qn = q + 1;
-                nx = qn < nb ? sinfo[qn] : make_int4(-1, 0, 0, 0);
-                load(min(qn, nb - 1), A);
-                if ((unsigned)(e - sh3) < (unsigned)W) fma8(B);
-                q = qn;
-                if (nx.x != grp) break;
-                sh3 = nx.z;
+                if (cq + 4 >= qe) {
+                    mma(A);
+                    break;
+                }
+                load(cq + 4, B);
+                mma(A);
+                cq += 4;
+                if (cq + 4 >= qe) {
+                    mma(B);
+                    break;
+                }
+                load(cq + 4, A);
+                mma(B);
+                cq += 4;
             }
+            q = qe;
+            if (q < nb) break;   // a new group starts inside the batch
+            advance();           // the group may continue into the next batch
+            q = 0;
+            if (nb <= 0 || sinfo[0].x != grp) break;
         }
         // flush the warp's plane of the window; cells outside the padded bin
         // carry zero sums (footprints lie inside)
-        const int zpl = a3 + e, xx = a1 + x;
-        if (zpl < p3 && xx < p1) {
-            double2 *col = buf + zpl * pstride + (a2 + rh) * p1 + xx;
+        // (all 8 loads first: the lane's cells are distinct, so no store can
+        // alias a later load, which the compiler cannot prove)
+        const int zpl = a3 + e;
+        if (zpl < p3 && !(dbg & 2)) {
+            double2 *pl = buf + zpl * pstride + (a2 + kp) * p1 + a1 + row;
+            bool ok[2][4];
+            double2 v[2][4];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                if (a2 + rh + i < p2) {
-                    double2 v = col[i * p1];
-                    v.x += acc[i].x;
-                    v.y += acc[i].y;
-                    col[i * p1] = v;
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                    ok[mt][nt] = a1 + mt * 8 + row < p1 && a2 + nt * 4 + kp < p2;
+                    v[mt][nt] = ok[mt][nt] ? pl[nt * 4 * p1 + mt * 8] : make_double2(0.0, 0.0);
                 }
-            }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt)
+                    if (ok[mt][nt])
+                        pl[nt * 4 * p1 + mt * 8] = make_double2(v[mt][nt].x + acc[mt][nt][0],
+                                                                v[mt][nt].y + acc[mt][nt][1]);
         }
     }
     __syncthreads();
     // merge with periodic wrap (Eq. 17): rows over warps, x over lanes
     const int o1 = corner[0] - h, o2 = corner[1] - h, o3 = corner[2] - h;
-    constexpr int NWARP = 16;
     int zz = 0, yy = warp;   // row r = zz p2 + yy, r = warp, warp + 16, ...
     while (yy >= p2) {
         yy -= p2;
         ++zz;
     }
     for (; zz < p3;) {
-        double2 *row = fine + ((int64_t)nk_wrap(o3 + zz, g.n[2]) * g.n[1] +
-                               nk_wrap(o2 + yy, g.n[1])) * (int64_t)g.n[0];
+        double2 *rowp = fine + ((int64_t)nk_wrap(o3 + zz, g.n[2]) * g.n[1] +
+                                nk_wrap(o2 + yy, g.n[1])) * (int64_t)g.n[0];
         const double2 *src = buf + (zz * p2 + yy) * p1;
-        for (int xx = lane; xx < p1; xx += 32) {
+        for (int xx = lane; xx < p1 && !(dbg & 1); xx += 32) {
             const double2 v = src[xx];
-            if (v.x != 0.0 || v.y != 0.0) nk_red(row + nk_wrap(o1 + xx, g.n[0]), v.x, v.y);
+            if (v.x != 0.0 || v.y != 0.0) nk_red(rowp + nk_wrap(o1 + xx, g.n[0]), v.x, v.y);
         }
         yy += NWARP;
         while (yy >= p2) {
@@ -602,9 +717,22 @@ int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
             NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
             int64_t stage_off = (p->max_pad_cells * (int64_t)sizeof(C) + 15) / 16 * 16;
+            // strengths in visit order (the kernel streams them by TMA)
+            const int64_t need = p->cap_M * p->ntrans;
+            if (need > p->cap_cvis || !p->d_cvis) {
+                if (p->d_cvis) cudaFree(p->d_cvis);
+                p->d_cvis = nullptr;
+                NK_CUDA(cudaMalloc(&p->d_cvis, 16 * (size_t)need));
+                p->cap_cvis = need;
+            }
+            k_gather_visit<<<dim3((M + 255) / 256, p->ntrans), 256, 0, p->stream>>>(
+                M, p->d_vperm, (const double2 *)c, g_M(p), (double2 *)p->d_cvis, p->cap_M);
+            NK_LAUNCH_CHECK();
+            ++*launches;
             kern<<<dim3((unsigned)p->S, p->ntrans), 512, smem, p->stream>>>(
-                p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm, (const double *)p->d_pts,
-                p->cap_M, (const double2 *)c, p->geom, (double2 *)fine, stage_off);
+                p->d_sub_bin, p->d_sub_start, p->d_sub_stop, (const double *)p->d_pts, p->cap_M,
+                (const double2 *)p->d_cvis, p->geom, (double2 *)fine, stage_off,
+                getenv("NK_DBG") ? atoi(getenv("NK_DBG")) : 0);
             NK_LAUNCH_CHECK();
             ++*launches;
             return NK_OK;

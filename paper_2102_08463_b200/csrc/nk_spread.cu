@@ -384,7 +384,7 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
         const double *ru = reinterpret_cast<const double *>(slot) + (b - (b & ~1));
         const double2 *rc = reinterpret_cast<const double2 *>(slot + 3 * RU * 8);
         nk_mbar_wait(mbar + k % 3, (k / 3) & 1);
-        const int v = lane * NWARP + warp;
+        const int v = (int)threadIdx.x;   // rows packed on the first warps
         if (v < nb * 3) {
             const int q = v / 3, ax = v - 3 * q;
             double k[W];

@@ -175,6 +175,22 @@ __device__ __forceinline__ void nk_mbar_wait(uint64_t *bar, unsigned parity) {
         : "memory");
 }
 
+// TMA bulk reduction shared -> global: dst[i] += src[i] for n complex
+// doubles (UBLKRED.G.S.ADD.F64), tracked in this thread's bulk group
+__device__ __forceinline__ void nk_bulk_red_add(double2 *dst, const double2 *src, int n) {
+    if (n <= 0) return;
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(
+                     dst),
+                 "r"(nk_smem_u32(src)), "r"(16 * n)
+                 : "memory");
+}
+// commit this thread's bulk operations and wait until their shared-memory
+// sources have been read (before the CTA may exit or reuse them)
+__device__ __forceinline__ void nk_bulk_wait_read() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 // Packed FMA with a broadcast constant addend: (a.x, a.y) * (b.x, b.y) + (c, c)
 // (sm_100 FFMA2 with a 32-bit immediate when c is a compile-time constant).
 __device__ __forceinline__ float2 nk_fma2_cc(float2 a, float2 b, float c) {

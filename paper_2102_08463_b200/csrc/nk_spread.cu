@@ -565,28 +565,28 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
                                                                 v[mt][nt].y + acc[mt][nt][1]);
         }
     }
+    // merge with periodic wrap (Eq. 17): one padded-bin row per thread as
+    // TMA bulk reductions (UBLKRED.ADD.F64) of its 1-2 contiguous segments
+    nk_fence_proxy_async();   // the flushes' generic stores before the async reads
     __syncthreads();
-    // merge with periodic wrap (Eq. 17): rows over warps, x over lanes
     const int o1 = corner[0] - h, o2 = corner[1] - h, o3 = corner[2] - h;
-    int zz = 0, yy = warp;   // row r = zz p2 + yy, r = warp, warp + 16, ...
-    while (yy >= p2) {
-        yy -= p2;
-        ++zz;
-    }
-    for (; zz < p3;) {
+    bool issued = false;
+    for (int r = threadIdx.x; r < p2 * p3 && !(dbg & 1); r += blockDim.x) {
+        const int zz = r / p2, yy = r - zz * p2;
         double2 *rowp = fine + ((int64_t)nk_wrap(o3 + zz, g.n[2]) * g.n[1] +
                                 nk_wrap(o2 + yy, g.n[1])) * (int64_t)g.n[0];
-        const double2 *src = buf + (zz * p2 + yy) * p1;
-        for (int xx = lane; xx < p1 && !(dbg & 1); xx += 32) {
-            const double2 v = src[xx];
-            if (v.x != 0.0 || v.y != 0.0) nk_red(rowp + nk_wrap(o1 + xx, g.n[0]), v.x, v.y);
+        const double2 *src = buf + r * p1;
+        // x = o1 + k wraps periodically: contiguous segments up to the seam
+        for (int k = 0; k < p1;) {
+            int x = (o1 + k) % g.n[0];
+            x += x < 0 ? g.n[0] : 0;
+            const int seg = min(p1 - k, g.n[0] - x);
+            nk_bulk_red_add(rowp + x, src + k, seg);
+            k += seg;
         }
-        yy += NWARP;
-        while (yy >= p2) {
-            yy -= p2;
-            ++zz;
-        }
+        issued = true;
     }
+    if (issued) nk_bulk_wait_read();
 }
 
 // K6c-2D: one warp per subproblem.  The warp owns the whole padded bin, so

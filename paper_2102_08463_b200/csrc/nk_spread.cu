@@ -384,36 +384,49 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
         const double *ru = reinterpret_cast<const double *>(slot) + (b - (b & ~1));
         const double2 *rc = reinterpret_cast<const double2 *>(slot + 3 * RU * 8);
         nk_mbar_wait(mbar + k % 3, (k / 3) & 1);
-        const int v = (int)threadIdx.x;   // rows packed on the first warps
-        if (v < nb * 3) {
-            const int q = v / 3, ax = v - 3 * q;
-            double k[W];
-            int t;
-            if (dbg & 8) {
-                t = (int)ceil(ru[ax * RU + q] - half) + h;
-#pragma unroll
-                for (int r = 0; r < W; ++r) k[r] = 0.5;
-            } else {
-                t = nk_kernel_row_poly<W>(ru[ax * RU + q], g, k) + h;
-            }
+        // a row's W values are split over 4 warps (pieces [part PP, part PP +
+        // PP)), each warp covering 32 rows, so the staging lag of a warp is a
+        // quarter of a row
+        constexpr int NPART = 4, PP = (W + NPART - 1) / NPART;
+        const int v = (int)threadIdx.x;
+        const int part = (v >> 5) & (NPART - 1);
+        const int rowi = ((v >> 7) << 5) | (v & 31);
+        if (rowi < nb * 3) {
+            const int q = rowi / 3, ax = rowi - 3 * q;
+            const double u = ru[ax * RU + q];
+            const double st = ceil(u - half);
+            const int t = (int)st + h;
             const int sh = t & TM;
-            if (ax == 2) {
-                const double2 cv = rc[q];
-                double2 *dst = sck3 + q;
+            const double d = st - u;
+            const double z0 = d * (2.0 / W), sp = fma(2.0, d, (double)(W - 1));
+            double2 cv = make_double2(0.0, 0.0);
+            if (ax == 2) cv = rc[q];
+            double *dst = (ax == 0 ? sk1 : sk2) + q;
+            double2 *dstc = sck3 + q;
+            typedef EsPoly64<W> P;
 #pragma unroll
-                for (int i = 0; i < WIN - W; ++i)
-                    dst[(i < sh ? i : i + W) * NB] = make_double2(0.0, 0.0);
+            for (int r = 0; r < W; ++r) {
+                if (r / PP != part) continue;   // warp-uniform
+                double kv;
+                if (r == 0 || r == W - 1) {
+                    kv = nk_es(z0 + (2.0 * r / W), g);
+                } else {
+                    kv = P::c(r - 1, P::D);
 #pragma unroll
-                for (int r = 0; r < W; ++r)
-                    dst[(sh + r) * NB] = make_double2(cv.x * k[r], cv.y * k[r]);
-            } else {
-                double *dst = (ax == 0 ? sk1 : sk2) + q;
-#pragma unroll
-                for (int i = 0; i < WIN - W; ++i) dst[(i < sh ? i : i + W) * KS] = 0.0;
-#pragma unroll
-                for (int r = 0; r < W; ++r) dst[(sh + r) * KS] = k[r];
+                    for (int kk = P::D - 1; kk >= 0; --kk) kv = fma(kv, sp, P::c(r - 1, kk));
+                }
+                if (ax == 2) dstc[(sh + r) * NB] = make_double2(cv.x * kv, cv.y * kv);
+                else dst[(sh + r) * KS] = kv;
             }
-            if (ax == 0) {
+            if (part == NPART - 1) {   // zeros outside the footprint
+#pragma unroll
+                for (int i = 0; i < WIN - W; ++i) {
+                    const int c0 = i < sh ? i : i + W;
+                    if (ax == 2) dstc[c0 * NB] = make_double2(0.0, 0.0);
+                    else dst[c0 * KS] = 0.0;
+                }
+            }
+            if (part == 0 && ax == 0) {
                 const double u2 = ru[RU + q], u3 = ru[2 * RU + q];
                 const int t2 = (int)ceil(u2 - half) + h, t3 = (int)ceil(u3 - half) + h;
                 sinfo[q] = make_int4(nk_start_code(t, t2, t3, p1, p2, g) >> (3 * L),

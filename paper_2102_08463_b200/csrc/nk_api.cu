@@ -310,7 +310,7 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     p->method = method;
     // footprint-start code space (setpts K4d): lexicographic in the padded
     // bin, or tile-major for the tiled f64 spread
-    const bool tiled = nk_spread_tiled(type, dim, precision, w, method);
+    const bool tiled = nk_tiled(type, dim, precision, w, method);
     const int tlg = tiled ? nk_tile_lg(w) : 0;
     p->start_space = p->max_pad_cells;
     if (tiled) {

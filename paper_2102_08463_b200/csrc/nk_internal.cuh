@@ -165,6 +165,15 @@ inline bool nk_spread_tiled(int type, int dim, int prec, int w, int method) {
     return type == 1 && dim == 3 && prec == NK_DOUBLE && w >= 9 && w <= 16 && method == NK_SM &&
            !getenv("NK_SPREAD_NO_TILE");
 }
+// Tiled f64 3D interpolation (K7t, nk_interp.cu): the adjoint of K6t on the
+// same tile groups (type 2, same plans).
+inline bool nk_interp_tiled(int type, int dim, int prec, int w, int method) {
+    return type == 2 && dim == 3 && prec == NK_DOUBLE && w >= 9 && w <= 16 && method == NK_SM &&
+           !getenv("NK_INTERP_NO_TILE");
+}
+inline bool nk_tiled(int type, int dim, int prec, int w, int method) {
+    return nk_spread_tiled(type, dim, prec, w, method) || nk_interp_tiled(type, dim, prec, w, method);
+}
 // Points staged per batch by the plane-owned 3D SM spread (nk_spread.cu):
 // 64 keeps the staging small enough for more resident CTAs (C3a spread
 // 1.24 -> 1.08 ms vs 128).
@@ -184,6 +193,13 @@ inline int64_t nk_sm_smem_bytes(int type, int dim, int prec, int w, const int *b
         b += 2 * ((int64_t)kTileBatch * (16 + 2 * kTileWin * rs + 2 * kTileWin * rs) +
                   2 * kTileWin * 4 * rs) +
              3 * (3 * (kTileBatch + 2) * rs + kTileBatch * 2 * rs) + 32;   // + TMA ring
+    else if (nk_interp_tiled(type, dim, prec, w, NK_SM))
+        // two buffers of: int4 info, k1 / k2 / k3 window rows (transposed,
+        // NB + 4 points per row), per-warp partial sums [16][NB] (complex);
+        // TMA ring of raw coordinates
+        b += 2 * ((int64_t)kTileBatch * 16 + 3 * kTileWin * (kTileBatch + 4) * rs +
+                  16 * kTileBatch * 2 * rs) +
+             3 * (3 * (kTileBatch + 2) * rs) + 32;
     else if (type == 1 && dim == 3)
         b += (int64_t)nk_sm3_batch(prec) *
              (((prec == NK_DOUBLE && w <= 16) ? 32 : w) * rs + 3 * w * rs + 16);
@@ -207,6 +223,7 @@ inline int64_t nk_sm_smem_bytes(int type, int dim, int prec, int w, const int *b
 inline int64_t nk_xwin_smem_bytes(int w) { return NK_XWIN_WARPS * NK_XWIN_NB * (16 + 3 * w * 8); }
 inline bool nk_interp_xwin(int type, int dim, int prec, int w, int method, int64_t max_sub_smem) {
     return type == 2 && dim == 3 && prec == NK_DOUBLE && w > 8 && method == NK_SM &&
+           !nk_interp_tiled(type, dim, prec, w, method) &&
            max_sub_smem + nk_xwin_smem_bytes(w) + 1024 <= 227 * 1024 &&
            !getenv("NK_INTERP_NO_XWIN");
 }

@@ -776,8 +776,10 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
             rc = order_by_start(p);   // composite key would exceed 32 bits
             if (rc) return rc;
         } else if (p->type == 2) {
+            // K7x / K7t group neighbours in footprint-start order
             const bool xwin = nk_interp_xwin(p->type, p->dim, p->prec, p->w, p->method,
-                                             p->max_sub_smem);
+                                             p->max_sub_smem) ||
+                              p->geom.tiled;
             bool interleave = !composite && p->prec == NK_DOUBLE && !xwin;
             if (xwin) {
                 // K7x groups neighbours in footprint-start order

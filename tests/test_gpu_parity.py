@@ -493,6 +493,7 @@ def test_xwin_interp_matches_per_thread_gather(nk, orc, dist, eps, monkeypatch):
     rounding, in both its start and its non-start visit orders, and direct
     sums (10 eps)."""
     modes, M = (24, 20, 16), 6000
+    monkeypatch.setenv("NK_INTERP_NO_TILE", "1")   # K7x, not the tiled K7t
     grid = orc.make_grid(modes, eps, "double")
     pts = orc.gen_points(dist, M, grid, 31, np.float64)
     rng = np.random.default_rng(5)
@@ -539,6 +540,32 @@ def test_tiled_spread_matches_plane_spread(nk, orc, dist, eps, bins, monkeypatch
     lay = orc.bin_sort(pts, orc.GridSpec(modes, p.grid.fine), p.bin_dims)
     assert np.array_equal(perm, lay.perm) and np.array_equal(starts, lay.starts)
     assert orc.rel_l2_error(got, orc.direct_type1(pts, c, modes)) < max(10 * eps, 1e-13)
+
+
+@pytest.mark.parametrize("dist,eps,bins", [("rand", 1e-12, None), ("cluster", 1e-9, None),
+                                           ("rand", 1e-11, (5, 3, 7)), ("gauss", 1e-15, None),
+                                           ("rand", 1e-8, (6, 6, 2))])
+def test_tiled_interp_matches_xwin(nk, orc, dist, eps, bins, monkeypatch):
+    """3D double type 2 with w >= 9 interpolates per tile group on the FP64
+    tensor cores (K7t: the adjoint of K6t).  Must match the x-window group
+    gather (K7x, NK_INTERP_NO_TILE=1) to rounding, with odd user bins
+    (partial tiles, edge bins), clustered points and w = 9 / 16, and direct
+    sums (10 eps)."""
+    modes, M = (24, 20, 16), 7001
+    grid = orc.make_grid(modes, eps, "double")
+    pts = orc.gen_points(dist, M, grid, 35, np.float64)
+    rng = np.random.default_rng(6)
+    f = rng.standard_normal(modes[::-1]) + 1j * rng.standard_normal(modes[::-1])
+    kw = {} if bins is None else {"bin_dims": bins}
+    p = nk.make_plan(2, modes, eps, "sm", "double", **kw)
+    p.set_points(pts)
+    got = p.execute(f)
+    monkeypatch.setenv("NK_INTERP_NO_TILE", "1")
+    q = nk.make_plan(2, modes, eps, "sm", "double", **kw)
+    q.set_points(pts)
+    ref = q.execute(f)
+    assert orc.rel_l2_error(got, ref) < 1e-14
+    assert orc.rel_l2_error(got, orc.direct_type2(pts, f, modes)) < max(10 * eps, 1e-13)
 
 
 @pytest.mark.parametrize("modes", [(128, 96), (512, 300), (1024, 40)])

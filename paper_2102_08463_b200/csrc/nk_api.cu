@@ -222,9 +222,11 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     // one-warp 2D spread (more warps in flight), 4096 for the staged
     // interpolation (one padded-bin load per bin).  Stage-level
     // build_subproblems keeps the reference default.
-    p->msub = opts.max_subproblem ? opts.max_subproblem
-                                  : (type == 2 ? 4096
-                                               : (dim == 2 ? 128 : 1024));
+    // (the tiled f64 3D interpolation, K7t, takes subproblems of <= 1024)
+    p->msub = opts.max_subproblem
+                  ? opts.max_subproblem
+                  : (type == 2 ? (dim == 3 && precision == NK_DOUBLE ? kTileMsub : 4096)
+                               : (dim == 2 ? 128 : 1024));
     if (p->msub < 1) {
         nk_set_error("max subproblem size must be >= 1, got " + std::to_string(p->msub));
         delete p;
@@ -279,7 +281,7 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
             return NK_ERR_VALUE;
         }
     }
-    int64_t need = nk_sm_smem_bytes(type, dim, precision, w, p->bin_dims, p->halo);
+    int64_t need = nk_sm_smem_bytes(type, dim, precision, w, p->bin_dims, p->halo, p->msub);
     if (method == NK_SM && need > smem_optin) {
         if (user_bins) {
             if (opts.method == NK_SM) {
@@ -294,7 +296,7 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
             while (need > smem_optin && (p->bin_dims[0] > 1 || p->bin_dims[1] > 1)) {
                 int ax = p->bin_dims[0] >= p->bin_dims[1] ? 0 : 1;
                 p->bin_dims[ax] = (p->bin_dims[ax] + 1) / 2;
-                need = nk_sm_smem_bytes(type, dim, precision, w, p->bin_dims, p->halo);
+                need = nk_sm_smem_bytes(type, dim, precision, w, p->bin_dims, p->halo, p->msub);
             }
             if (need > smem_optin) method = NK_GMSORT;
             p->nbins = 1;
@@ -310,7 +312,7 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     p->method = method;
     // footprint-start code space (setpts K4d): lexicographic in the padded
     // bin, or tile-major for the tiled f64 spread
-    const bool tiled = nk_tiled(type, dim, precision, w, method);
+    const bool tiled = nk_tiled(type, dim, precision, w, method, p->msub);
     const int tlg = tiled ? nk_tile_lg(w) : 0;
     p->start_space = p->max_pad_cells;
     if (tiled) {

@@ -160,6 +160,7 @@ constexpr int kTileWin = 16;
 #define NK_TILE_NB 32
 #endif
 constexpr int kTileBatch = NK_TILE_NB;   // points per staged batch (two buffers)
+constexpr int kTileMsub = 1024;          // max subproblem of the tiled interp (chunk table)
 constexpr int nk_tile_lg(int w) { return w + 7 <= kTileWin ? 3 : (w + 3 <= kTileWin ? 2 : (w + 1 <= kTileWin ? 1 : 0)); }
 inline bool nk_spread_tiled(int type, int dim, int prec, int w, int method) {
     return type == 1 && dim == 3 && prec == NK_DOUBLE && w >= 9 && w <= 16 && method == NK_SM &&
@@ -167,12 +168,13 @@ inline bool nk_spread_tiled(int type, int dim, int prec, int w, int method) {
 }
 // Tiled f64 3D interpolation (K7t, nk_interp.cu): the adjoint of K6t on the
 // same tile groups (type 2, same plans).
-inline bool nk_interp_tiled(int type, int dim, int prec, int w, int method) {
+inline bool nk_interp_tiled(int type, int dim, int prec, int w, int method, int msub = 0) {
     return type == 2 && dim == 3 && prec == NK_DOUBLE && w >= 9 && w <= 16 && method == NK_SM &&
-           !getenv("NK_INTERP_NO_TILE");
+           msub <= kTileMsub && !getenv("NK_INTERP_NO_TILE");
 }
-inline bool nk_tiled(int type, int dim, int prec, int w, int method) {
-    return nk_spread_tiled(type, dim, prec, w, method) || nk_interp_tiled(type, dim, prec, w, method);
+inline bool nk_tiled(int type, int dim, int prec, int w, int method, int msub) {
+    return nk_spread_tiled(type, dim, prec, w, method) ||
+           nk_interp_tiled(type, dim, prec, w, method, msub);
 }
 // Points staged per batch by the plane-owned 3D SM spread (nk_spread.cu):
 // 64 keeps the staging small enough for more resident CTAs (C3a spread
@@ -181,7 +183,7 @@ inline int nk_sm3_batch(int prec) { return 64; }
 // Dynamic shared memory (bytes) of the SM spread / staged interp for a plan
 // shape: padded bin (+ point staging for the 3D spread).
 inline int64_t nk_sm_smem_bytes(int type, int dim, int prec, int w, const int *bin_dims,
-                                int halo) {
+                                int halo, int msub) {
     int64_t cells = 1;
     for (int i = 0; i < dim; ++i) cells *= bin_dims[i] + 2 * halo;
     int64_t rs = prec == NK_DOUBLE ? 8 : 4;
@@ -193,13 +195,9 @@ inline int64_t nk_sm_smem_bytes(int type, int dim, int prec, int w, const int *b
         b += 2 * ((int64_t)kTileBatch * (16 + 2 * kTileWin * rs + 2 * kTileWin * rs) +
                   2 * kTileWin * 4 * rs) +
              3 * (3 * (kTileBatch + 2) * rs + kTileBatch * 2 * rs) + 32;   // + TMA ring
-    else if (nk_interp_tiled(type, dim, prec, w, NK_SM))
-        // two buffers of: int4 info, k1 / k2 / k3 window rows (transposed,
-        // NB + 4 points per row), per-warp partial sums [16][NB] (complex);
-        // TMA ring of raw coordinates
-        b += 2 * ((int64_t)kTileBatch * 16 + 3 * kTileWin * (kTileBatch + 4) * rs +
-                  16 * kTileBatch * 2 * rs) +
-             3 * (3 * (kTileBatch + 2) * rs) + 32;
+    else if (nk_interp_tiled(type, dim, prec, w, NK_SM, msub))
+        // per warp (16): kernel rows [3][16][8] doubles; chunk starts
+        b += 16 * 3 * kTileWin * 8 * rs + 4 * (int64_t)(kTileMsub + 1);
     else if (type == 1 && dim == 3)
         b += (int64_t)nk_sm3_batch(prec) *
              (((prec == NK_DOUBLE && w <= 16) ? 32 : w) * rs + 3 * w * rs + 16);
@@ -223,7 +221,6 @@ inline int64_t nk_sm_smem_bytes(int type, int dim, int prec, int w, const int *b
 inline int64_t nk_xwin_smem_bytes(int w) { return NK_XWIN_WARPS * NK_XWIN_NB * (16 + 3 * w * 8); }
 inline bool nk_interp_xwin(int type, int dim, int prec, int w, int method, int64_t max_sub_smem) {
     return type == 2 && dim == 3 && prec == NK_DOUBLE && w > 8 && method == NK_SM &&
-           !nk_interp_tiled(type, dim, prec, w, method) &&
            max_sub_smem + nk_xwin_smem_bytes(w) + 1024 <= 227 * 1024 &&
            !getenv("NK_INTERP_NO_XWIN");
 }

@@ -401,16 +401,17 @@ k_interp_xwin(int S, const int32_t *__restrict__ sub_bin, const int32_t *__restr
 // K7t: tiled f64 3D interpolation on the FP64 tensor cores -- the adjoint
 // of K6t (nk_spread.cu) on the same tile groups (setpts: tile-major
 // footprint-start order).  The padded bin is copied into shared memory
-// (cp.async, periodic wrap); the coordinates of the subproblem stream in by
-// TMA bulk copies (3-slot mbarrier ring) and are staged as pre-shifted
-// window rows (transposed [cell][point]).  For a group, warp = window plane
-// e: it holds its plane's 16 x 16 window as DMMA A fragments (rows (y,
-// re|im), columns x) and, per chunk of 8 points,
-//   V[(y, c)][p] = sum_x G_e[x][y]_c k1_p[x]          (16 DMMA m8n8k4)
-//   T_e[p]_c     = sum_y V[(y, c)][p] k2_p[y]         (DFMA + 2 shuffles)
-// then k3_p[e] T_e[p] goes to a per-warp partial-sum table; after the
-// batch barrier every point's 16 plane sums are added and stored to its
-// input slot.
+// (cp.async, periodic wrap) while warp 0 cuts the subproblem into chunks:
+// runs of <= 8 consecutive points of one start tile.  Interpolation only
+// reads the bin, so warps then work independently (no barriers): a warp
+// takes a chunk, evaluates its points' kernel rows into a private table
+// (pre-shifted into the tile's 16 x 16 x 16 window, zeros outside the
+// footprint), and for each window plane e runs one small GEMM on the DMMA
+// units,
+//   V_e[(y, c)][p] = sum_x G[e][y][x]_c k1_p[x]       (16 DMMA m8n8k4),
+// contracts it with k2_p[y] and k3_p[e] in registers, and finally sums
+// over its lanes (2 shuffles) and stores each point's value to its input
+// slot.  Planes outside every chunk point's footprint (k3 = 0) are skipped.
 template <int W>
 __global__ void __launch_bounds__(512, 1)
 k_interp_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
@@ -418,22 +419,19 @@ k_interp_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
                const double *__restrict__ pts, int64_t pitch,
                const double2 *__restrict__ fine, Geom g, double2 *__restrict__ out,
                int64_t stage_off) {
-    constexpr int WIN = kTileWin, NB = kTileBatch, L = nk_tile_lg(W), TM = (1 << L) - 1;
-    constexpr int NWARP = 16, KS = NB + 4;
+    constexpr int WIN = kTileWin, L = nk_tile_lg(W), TM = (1 << L) - 1, NWARP = 16;
+    // staged rows: [3 axes][16 cells][8 points], point slot swizzled by cell
+    // bit 1 (conflict-free B fragment and epilogue reads)
+    constexpr int CS = 8;
+    auto pos = [](int c, int q) { return c * CS + (q ^ (((c >> 1) & 1) << 2)); };
     static_assert(W + TM <= WIN, "window too small for the tile");
-    static_assert(NB <= 32, "one boundary mask word per batch");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2 *buf = reinterpret_cast<double2 *>(smem_raw);
-    unsigned char *stg = smem_raw + stage_off;
-    // two staging buffers {info [NB], k1 / k2 / k3 rows [16][KS]}, two
-    // partial-sum tables [16 warps][NB] (complex), the raw TMA ring
-    constexpr int SB = NB * 16 + 3 * WIN * KS * 8;
-    auto sinfo_of = [&](int bi) { return reinterpret_cast<int4 *>(stg + bi * SB); };
-    auto sk1_of = [&](int bi) { return reinterpret_cast<double *>(stg + bi * SB + NB * 16); };
-    double2 *red0 = reinterpret_cast<double2 *>(stg + 2 * SB);
-    constexpr int RU = NB + 2, RB = 3 * RU * 8;
-    unsigned char *raw = stg + 2 * SB + 2 * NWARP * NB * 16;
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(raw + 3 * RB);
+    // per warp: k1 / k2 / k3 rows [3][16 cells][CS]; chunk starts
+    double *wst = reinterpret_cast<double *>(smem_raw + stage_off) +
+                  (threadIdx.x >> 5) * (3 * WIN * CS);
+    int *cstart = reinterpret_cast<int *>(smem_raw + stage_off) + 2 * NWARP * 3 * WIN * CS;
+    __shared__ int sh_nchunk;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x;
     fine += blockIdx.y * g.ntot;
@@ -449,185 +447,126 @@ k_interp_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
     nk_cp_async_commit();
     const double half = 0.5 * W;
     const int j0 = sub_start[s], j1 = sub_stop[s];
-    auto issue = [&](int k) {
-        const int b = j0 + k * NB, nb = min(NB, j1 - b);
-        if (nb <= 0) return;
-        unsigned char *slot = raw + (k % 3) * RB;
-        const int b0 = b & ~1;
-        const unsigned ub = (unsigned)(((b + nb - b0) + 1) & ~1) * 8u;
-        nk_fence_proxy_async();
-        nk_mbar_expect_tx(mbar + k % 3, 3 * ub);
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax)
-            nk_bulk_g2s(slot + ax * RU * 8, pts + ax * pitch + b0, ub, mbar + k % 3);
+    auto tile_of = [&](int j) {
+        const int t1 = (int)ceil(__ldg(pts + j) - half) + h;
+        const int t2 = (int)ceil(__ldg(pts + pitch + j) - half) + h;
+        const int t3 = (int)ceil(__ldg(pts + 2 * pitch + j) - half) + h;
+        return nk_start_code(t1, t2, t3, p1, p2, g) >> (3 * L);
     };
-    // window rows of batch k into staging buffer bi (entry i = k_axis[i - sh],
-    // zeros outside the footprint), split over 4 warps per 32 rows
-    auto stage = [&](int k, int bi) {
-        const int b = j0 + k * NB, nb = min(NB, j1 - b);
-        int4 *sinfo = sinfo_of(bi);
-        double *sk = sk1_of(bi);
-        const double *ru = reinterpret_cast<const double *>(raw + (k % 3) * RB) + (b - (b & ~1));
-        nk_mbar_wait(mbar + k % 3, (k / 3) & 1);
-        constexpr int NPART = 4, PP = (W + NPART - 1) / NPART;
-        const int v = (int)threadIdx.x;
-        const int part = (v >> 5) & (NPART - 1);
-        const int rowi = ((v >> 7) << 5) | (v & 31);
-        if (rowi < nb * 3) {
-            const int q = rowi / 3, ax = rowi - 3 * q;
-            const double u = ru[ax * RU + q];
-            const double st = ceil(u - half);
-            const int t = (int)st + h;
-            const int sh = t & TM;
-            const double d = st - u;
-            const double z0 = d * (2.0 / W), sp = fma(2.0, d, (double)(W - 1));
-            double *dst = sk + ax * WIN * KS + q;
-            typedef EsPoly64<W> P;
-#pragma unroll
-            for (int r = 0; r < W; ++r) {
-                if (r / PP != part) continue;   // warp-uniform
-                double kv;
-                if (r == 0 || r == W - 1) {
-                    kv = nk_es(z0 + (2.0 * r / W), g);
-                } else {
-                    kv = P::c(r - 1, P::D);
-#pragma unroll
-                    for (int kk = P::D - 1; kk >= 0; --kk) kv = fma(kv, sp, P::c(r - 1, kk));
-                }
-                dst[(sh + r) * KS] = kv;
-            }
-            if (part == NPART - 1) {
-#pragma unroll
-                for (int i = 0; i < WIN - W; ++i) dst[(i < sh ? i : i + W) * KS] = 0.0;
-            }
-            if (part == 0 && ax == 0) {
-                const double u2 = ru[RU + q], u3 = ru[2 * RU + q];
-                const int t2 = (int)ceil(u2 - half) + h, t3 = (int)ceil(u3 - half) + h;
-                sinfo[q] = make_int4(nk_start_code(t, t2, t3, p1, p2, g) >> (3 * L),
-                                     (t & ~TM) | ((t2 & ~TM) << 8) | ((t3 & ~TM) << 16),
-                                     t3 & TM, 0);
-            }
+    if (warp == 0) {
+        // chunks: a point starts one if its tile differs from its
+        // predecessor's or it is 8 points past its group's start
+        int gs = j0, nc = 0, prev = -1;
+        for (int base = j0; base < j1; base += 32) {
+            const int j = base + lane;
+            const int tl = j < j1 ? tile_of(j) : -2;
+            const int tp = __shfl_up_sync(0xffffffffu, tl, 1);
+            const bool f = j < j1 && (lane == 0 ? tl != prev : tl != tp);
+            const unsigned fm = __ballot_sync(0xffffffffu, f);
+            // latest group start at or below this lane
+            const unsigned below = fm & (0xffffffffu >> (31 - lane));
+            const int g_at = below ? base + 31 - __clz(below) : gs;
+            const bool cst = j < j1 && ((j - g_at) & 7) == 0;
+            const unsigned cm = __ballot_sync(0xffffffffu, cst);
+            if (cst) cstart[nc + __popc(cm & ((1u << lane) - 1u))] = j;
+            nc += __popc(cm);
+            gs = fm ? base + 31 - __clz(fm) : gs;
+            prev = __shfl_sync(0xffffffffu, tl, 31);
         }
-    };
-    // sum the 16 plane partials of batch k's points and store them
-    auto finish = [&](int k) {
-        const int b = j0 + k * NB, nb = min(NB, j1 - b);
-        const double *red = reinterpret_cast<const double *>(red0 + (k & 1) * NWARP * NB);
-        const int t = threadIdx.x;
-        if (t < 2 * nb) {
-            const int q = t >> 1, cpart = t & 1;
-            double acc = 0.0;
-#pragma unroll
-            for (int w = 0; w < NWARP; ++w) acc += red[(w * NB + q) * 2 + cpart];
-            reinterpret_cast<double *>(out + __ldcs(perm + b + q))[cpart] = acc;
+        if (lane == 0) {
+            cstart[nc] = j1;
+            sh_nchunk = nc;
         }
-    };
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int i = 0; i < 3; ++i) nk_mbar_init(mbar + i, 1);
-        nk_fence_mbar_init();
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        issue(0);
-        issue(1);
-        issue(2);
-    }
-    int kb = 0;
-    int nb = min(NB, j1 - j0);
-    if (nb > 0) stage(0, 0);
     nk_cp_async_wait<0>();
-    __syncthreads();   // batch 0 staged, padded bin in shared memory
-    if (j1 - j0 > NB) stage(1, 1);
-    const int4 *sinfo = sinfo_of(0);
-    const double *sk1 = sk1_of(0);
-    unsigned bnd = 0;
-    auto boundaries = [&]() {
-        const int ga = lane < nb ? sinfo[lane].x : -1;
-        const int pa = __shfl_up_sync(0xffffffffu, ga, 1);
-        bnd = __ballot_sync(0xffffffffu, lane < nb && (lane == 0 || ga != pa));
-    };
-    auto advance = [&]() {
-        __syncthreads();   // batch kb's partials complete; batch kb + 1 staged
-        finish(kb);
-        ++kb;
-        nb = min(NB, j1 - (j0 + kb * NB));
-        if (threadIdx.x == 0) issue(kb + 2);
-        if (j1 - (j0 + (kb + 1) * NB) > 0) stage(kb + 1, (kb + 1) & 1);
-        sinfo = sinfo_of(kb & 1);
-        sk1 = sk1_of(kb & 1);
-        if (nb > 0) boundaries();
-    };
-    if (nb > 0) boundaries();
+    __syncthreads();   // padded bin and chunk list ready
+    const int nchunk = sh_nchunk;
     const int kx = lane & 3, prow = lane >> 2, ylane = lane >> 3, cpart = (lane >> 2) & 1;
-    int q = 0;
-    while (nb > 0) {
-        const int4 g0 = sinfo[q];
-        const int grp = g0.x;
-        const int a1 = g0.y & 0xff, a2 = (g0.y >> 8) & 0xff, a3 = g0.y >> 16;
-        const int e = (warp - a3) & (WIN - 1);   // the warp's window plane
-        const int zpl = a3 + e;
-        // A fragments: A[(y, c)][x] = G[zpl][a2 + y][a1 + x]_c, row (y, c) =
-        // mt * 8 + lane / 4, column x = ks * 4 + lane % 4
-        double af[4][4];
-        {
-            const double *pl = reinterpret_cast<const double *>(buf + zpl * pstride) + cpart;
+    double *sk1 = wst, *sk2 = wst + WIN * CS, *sk3 = wst + 2 * WIN * CS;
+    for (int ch = warp; ch < nchunk; ch += NWARP) {
+        const int cs = cstart[ch], n = cstart[ch + 1] - cs;   // 1..8 points, one tile
+        // kernel rows: lane (q, axis) for q < n, window-shifted, transposed
+        int t0 = 0;
+        if (lane < 3 * n) {
+            const int q = lane / 3, ax = lane - 3 * q;
+            double k[W];
+            const int t = nk_kernel_row_poly<W>(__ldg(pts + ax * pitch + cs + q), g, k) + h;
+            const int sh = t & TM;
+            double *dst = wst + ax * WIN * CS;
+#pragma unroll
+            for (int i = 0; i < WIN - W; ++i) dst[pos(i < sh ? i : i + W, q)] = 0.0;
+#pragma unroll
+            for (int r = 0; r < W; ++r) dst[pos(sh + r, q)] = k[r];
+            t0 = t & ~TM;
+        }
+        // the chunk's window anchor (any point's tile corner: lanes 0-2)
+        const int a1 = __shfl_sync(0xffffffffu, t0, 0);
+        const int a2 = __shfl_sync(0xffffffffu, t0, 1);
+        const int a3 = __shfl_sync(0xffffffffu, t0, 2);
+        // zero rows of the unused point columns (n..7) so B / k2 / k3 are 0
+        for (int v = lane; v < 3 * WIN * (8 - n); v += 32) {
+            const int c = v / (8 - n), q = n + (v - c * (8 - n));
+            wst[(c / WIN) * WIN * CS + pos(c % WIN, q)] = 0.0;
+        }
+        __syncwarp();
+        // B[x][p] = k1_p[x] (x = ks * 4 + lane % 4, p = lane / 4)
+        double bf[4];
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) bf[ks] = sk1[pos(ks * 4 + kx, prow)];
+        // k2_p[y] for the lane's epilogue rows y = mt * 4 + lane / 8 and
+        // points 2 (lane % 4) + {0, 1}
+        double k2a[4], k2b[4];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            k2a[mt] = sk2[pos(mt * 4 + ylane, 2 * kx)];
+            k2b[mt] = sk2[pos(mt * 4 + ylane, 2 * kx + 1)];
+        }
+        double acc0 = 0.0, acc1 = 0.0;
+        const double *plane0 = reinterpret_cast<const double *>(buf) + cpart;
+#pragma unroll 1
+        for (int e = 0; e < WIN; ++e) {
+            const int zpl = a3 + e;
+            const double k3a = sk3[pos(e, 2 * kx)], k3b = sk3[pos(e, 2 * kx + 1)];
+            if (zpl >= p3 || !__any_sync(0xffffffffu, k3a != 0.0 || k3b != 0.0)) continue;
+            // A[(y, c)][x] = G[zpl][a2 + y][a1 + x]_c, row (y, c) = mt * 8 +
+            // lane / 4, column x = ks * 4 + lane % 4
+            const double *pl = plane0 + 2 * zpl * pstride;
+            double af[4][4];
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
                     const int xx = a1 + ks * 4 + kx, yy = a2 + mt * 4 + ylane;
-                    af[mt][ks] = (zpl < p3 && xx < p1 && yy < p2) ? pl[2 * (yy * p1 + xx)] : 0.0;
+                    af[mt][ks] = (xx < p1 && yy < p2) ? pl[2 * (yy * p1 + xx)] : 0.0;
                 }
-        }
-        for (;;) {
-            const unsigned rest = q + 1 < 32 ? bnd >> (q + 1) : 0u;
-            const int qe = rest ? min(nb, q + __ffs(rest)) : nb;
-            const double *sk2 = sk1 + WIN * KS, *sk3 = sk2 + WIN * KS;
-            double *red = reinterpret_cast<double *>(red0 + (kb & 1) * NWARP * NB);
-            for (int cq = q; cq < qe; cq += 8) {
-                // B[x][p] = k1_p[x]: lane holds x = ks * 4 + lane % 4, p = lane / 4
-                const int qb = min(cq + prow, nb - 1);
-                double bf[4];
+            double cacc[4][2];
 #pragma unroll
-                for (int ks = 0; ks < 4; ++ks) bf[ks] = sk1[(ks * 4 + kx) * KS + qb];
-                double cacc[4][2];
+            for (int mt = 0; mt < 4; ++mt) cacc[mt][0] = cacc[mt][1] = 0.0;
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) {
-                    cacc[mt][0] = cacc[mt][1] = 0.0;
+            for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
-                    for (int ks = 0; ks < 4; ++ks)
-                        nk_dmma(cacc[mt][0], cacc[mt][1], af[mt][ks], bf[ks]);
-                }
-                // C[(y, c)][p]: lane row (y = mt * 4 + lane / 8, c), columns
-                // p = 2 (lane % 4) + {0, 1}; contract y with k2_p[y]
-                const int pa = cq + 2 * kx;
-                const int qa = min(pa, nb - 1), qc = min(pa + 1, nb - 1);
-                double v0 = 0.0, v1 = 0.0;
+                for (int mt = 0; mt < 4; ++mt) nk_dmma(cacc[mt][0], cacc[mt][1], af[mt][ks], bf[ks]);
+            double v0 = 0.0, v1 = 0.0;
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) {
-                    const int yy = mt * 4 + ylane;
-                    v0 = fma(cacc[mt][0], sk2[yy * KS + qa], v0);
-                    v1 = fma(cacc[mt][1], sk2[yy * KS + qc], v1);
-                }
-                v0 += __shfl_xor_sync(0xffffffffu, v0, 8);
-                v1 += __shfl_xor_sync(0xffffffffu, v1, 8);
-                v0 += __shfl_xor_sync(0xffffffffu, v0, 16);
-                v1 += __shfl_xor_sync(0xffffffffu, v1, 16);
-                if (ylane == 0) {   // lanes 0-7: points pa, pa + 1, component c
-                    if (pa < qe) red[(warp * NB + pa) * 2 + cpart] = v0 * sk3[e * KS + qa];
-                    if (pa + 1 < qe) red[(warp * NB + pa + 1) * 2 + cpart] = v1 * sk3[e * KS + qc];
-                }
+            for (int mt = 0; mt < 4; ++mt) {
+                v0 = fma(cacc[mt][0], k2a[mt], v0);
+                v1 = fma(cacc[mt][1], k2b[mt], v1);
             }
-            q = qe;
-            if (q < nb) break;   // a new group starts inside the batch
-            advance();           // the group may continue into the next batch
-            q = 0;
-            if (nb <= 0 || sinfo[0].x != grp) break;
+            acc0 = fma(k3a, v0, acc0);
+            acc1 = fma(k3b, v1, acc1);
         }
+        acc0 += __shfl_xor_sync(0xffffffffu, acc0, 8);
+        acc1 += __shfl_xor_sync(0xffffffffu, acc1, 8);
+        acc0 += __shfl_xor_sync(0xffffffffu, acc0, 16);
+        acc1 += __shfl_xor_sync(0xffffffffu, acc1, 16);
+        if (ylane == 0) {   // lanes 0-7: points 2 (lane % 4) + {0, 1}, component c
+            const int pa = 2 * kx;
+            if (pa < n) reinterpret_cast<double *>(out + __ldcs(perm + cs + pa))[cpart] = acc0;
+            if (pa + 1 < n)
+                reinterpret_cast<double *>(out + __ldcs(perm + cs + pa + 1))[cpart] = acc1;
+        }
+        __syncwarp();   // the staged rows are reused by the warp's next chunk
     }
-    __syncthreads();
-    finish(kb);
 }
 
 template <typename T, int D, int W>

@@ -408,8 +408,11 @@ k_interp_xwin(int S, const int32_t *__restrict__ sub_bin, const int32_t *__restr
 // (pre-shifted into the tile's 16 x 16 x 16 window, zeros outside the
 // footprint), and for each window plane e runs one small GEMM on the DMMA
 // units,
-//   V_e[(y, c)][p] = sum_x G[e][y][x]_c k1_p[x]       (16 DMMA m8n8k4),
-// contracts it with k2_p[y] and k3_p[e] in registers, and finally sums
+//   V[(x, c)][p] += sum_y G[e][y][x]_c (k2_p[y] k3_p[e])   (16 DMMA m8n8k4)
+// (y as the reduction index: a half-warp's A fragment is 2 x-cells x 4 rows
+// x re|im, conflict-free for the 22-cell padded rows of the default bins;
+// k3 folded into B so all planes share the accumulators), then contracts
+// x with k1_p[x] in registers and sums
 // over its lanes (2 shuffles) and stores each point's value to its input
 // slot.  Planes outside every chunk point's footprint (k3 = 0) are skipped.
 template <int W>
@@ -509,51 +512,47 @@ k_interp_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
             wst[(c / WIN) * WIN * CS + pos(c % WIN, q)] = 0.0;
         }
         __syncwarp();
-        // B[x][p] = k1_p[x] (x = ks * 4 + lane % 4, p = lane / 4)
+        // B_e[y][p] = k2_p[y] k3_p[e] (y = ks * 4 + lane % 4, p = lane / 4):
+        // with k3 folded into B every plane accumulates into the same DMMA
+        // tiles, V[(x, c)][p] = sum_e sum_y G[e][y][x]_c k2_p[y] k3_p[e]
         double bf[4];
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) bf[ks] = sk1[pos(ks * 4 + kx, prow)];
-        // k2_p[y] for the lane's epilogue rows y = mt * 4 + lane / 8 and
-        // points 2 (lane % 4) + {0, 1}
-        double k2a[4], k2b[4];
+        for (int ks = 0; ks < 4; ++ks) bf[ks] = sk2[pos(ks * 4 + kx, prow)];
+        double cacc[4][2];
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-            k2a[mt] = sk2[pos(mt * 4 + ylane, 2 * kx)];
-            k2b[mt] = sk2[pos(mt * 4 + ylane, 2 * kx + 1)];
-        }
-        double acc0 = 0.0, acc1 = 0.0;
+        for (int mt = 0; mt < 4; ++mt) cacc[mt][0] = cacc[mt][1] = 0.0;
         const double *plane0 = reinterpret_cast<const double *>(buf) + cpart;
+        const int e_end = min(WIN, p3 - a3);
 #pragma unroll 1
-        for (int e = 0; e < WIN; ++e) {
-            const int zpl = a3 + e;
-            const double k3a = sk3[pos(e, 2 * kx)], k3b = sk3[pos(e, 2 * kx + 1)];
-            if (zpl >= p3 || !__any_sync(0xffffffffu, k3a != 0.0 || k3b != 0.0)) continue;
-            // A[(y, c)][x] = G[zpl][a2 + y][a1 + x]_c, row (y, c) = mt * 8 +
-            // lane / 4, column x = ks * 4 + lane % 4
-            const double *pl = plane0 + 2 * zpl * pstride;
+        for (int e = 0; e < e_end; ++e) {
+            const double k3v = sk3[pos(e, prow)];
+            if (!__any_sync(0xffffffffu, k3v != 0.0)) continue;   // outside every footprint
+            // A[(x, c)][y] = G[a3 + e][a2 + y][a1 + x]_c, row (x, c) = mt * 8 +
+            // lane / 4, column y = ks * 4 + lane % 4
+            const double *pl = plane0 + 2 * (a3 + e) * pstride;
             double af[4][4];
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
-                    const int xx = a1 + ks * 4 + kx, yy = a2 + mt * 4 + ylane;
+                    const int xx = a1 + mt * 4 + ylane, yy = a2 + ks * 4 + kx;
                     af[mt][ks] = (xx < p1 && yy < p2) ? pl[2 * (yy * p1 + xx)] : 0.0;
                 }
-            double cacc[4][2];
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt) cacc[mt][0] = cacc[mt][1] = 0.0;
+            for (int ks = 0; ks < 4; ++ks) {
+                const double bv = bf[ks] * k3v;
 #pragma unroll
-            for (int ks = 0; ks < 4; ++ks)
-#pragma unroll
-                for (int mt = 0; mt < 4; ++mt) nk_dmma(cacc[mt][0], cacc[mt][1], af[mt][ks], bf[ks]);
-            double v0 = 0.0, v1 = 0.0;
-#pragma unroll
-            for (int mt = 0; mt < 4; ++mt) {
-                v0 = fma(cacc[mt][0], k2a[mt], v0);
-                v1 = fma(cacc[mt][1], k2b[mt], v1);
+                for (int mt = 0; mt < 4; ++mt)
+                    nk_dmma(cacc[mt][0], cacc[mt][1], af[mt][ks], bv);
             }
-            acc0 = fma(k3a, v0, acc0);
-            acc1 = fma(k3b, v1, acc1);
+        }
+        // C[(x, c)][p]: lane rows x = mt * 4 + lane / 8 (component c), points
+        // 2 (lane % 4) + {0, 1}; contract x with k1_p[x]
+        double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            acc0 = fma(cacc[mt][0], sk1[pos(mt * 4 + ylane, 2 * kx)], acc0);
+            acc1 = fma(cacc[mt][1], sk1[pos(mt * 4 + ylane, 2 * kx + 1)], acc1);
         }
         acc0 += __shfl_xor_sync(0xffffffffu, acc0, 8);
         acc1 += __shfl_xor_sync(0xffffffffu, acc1, 8);

@@ -9,6 +9,8 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "nk_internal.cuh"
 
 namespace {
@@ -375,6 +377,36 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
         return fail(NK_ERR_MEMORY);                                                 \
     }
     NK_ALLOC(p->d_fine, p->n_tot * p->csize * p->ntrans);
+    // TMA tensor map of the fine grid for the tiled interpolation: one
+    // cp.async.bulk.tensor box per (non-wrapping) padded bin
+    if (p->geom.tiled && type == 2) {
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+        if (!encode) {
+            cudaDriverEntryPointQueryResult q;
+            void *fn = nullptr;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+                    cudaSuccess &&
+                q == cudaDriverEntryPointSuccess)
+                encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+            cudaGetLastError();
+        }
+        const int h2 = 2 * p->halo;
+        const cuuint64_t dims[4] = {(cuuint64_t)(2 * p->n[0]), (cuuint64_t)p->n[1],
+                                    (cuuint64_t)p->n[2], (cuuint64_t)p->ntrans};
+        const cuuint64_t strides[3] = {(cuuint64_t)(16 * p->n[0]),
+                                       (cuuint64_t)(16 * p->n[0] * p->n[1]),
+                                       (cuuint64_t)(16 * p->n_tot)};
+        const cuuint32_t box[4] = {(cuuint32_t)(2 * (p->bin_dims[0] + h2)),
+                                   (cuuint32_t)(p->bin_dims[1] + h2),
+                                   (cuuint32_t)(p->bin_dims[2] + h2), 1};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        p->tmap_ok = encode && box[0] <= 256 && box[1] <= 256 && box[2] <= 256 &&
+                     (box[0] * 8) % 16 == 0 &&
+                     encode(&p->tmap_fine, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, p->d_fine, dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
     NK_ALLOC(p->d_corr, corr.size() * p->csize / 2);
     NK_ALLOC(p->d_counts, 4 * p->nbins);
     NK_ALLOC(p->d_starts, 4 * (p->nbins + 1));

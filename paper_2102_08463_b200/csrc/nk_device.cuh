@@ -191,6 +191,18 @@ __device__ __forceinline__ void nk_bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
+// 4D TMA tensor copy global -> shared (box of the tensor map at
+// coordinates c0..c3, innermost first), completion on the mbarrier (UTMALDG)
+__device__ __forceinline__ void nk_tma_load_4d(void *dst, const CUtensorMap *map, int c0, int c1,
+                                               int c2, int c3, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(nk_smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+        "r"(nk_smem_u32(bar))
+        : "memory");
+}
+
 // Packed FMA with a broadcast constant addend: (a.x, a.y) * (b.x, b.y) + (c, c)
 // (sm_100 FFMA2 with a 32-bit immediate when c is a compile-time constant).
 __device__ __forceinline__ float2 nk_fma2_cc(float2 a, float2 b, float c) {

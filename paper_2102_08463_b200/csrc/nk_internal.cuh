@@ -1,6 +1,7 @@
 // Internal declarations shared by the libnufft_b200 translation units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cufft.h>
 #include <stdint.h>
@@ -91,6 +92,10 @@ struct nk_plan {
     void *d_twiddle;        // n_1 complex exp(+2 pi i k / n_1)
     int *d_work;            // n_trans work counters of the staged interpolation
     void *d_cvis;           // strengths gathered into visit order (tiled f64 spread)
+    // TMA descriptor of d_fine as doubles (2 n1, n2, n3, n_trans) with the
+    // full padded bin as its box (tiled f64 interpolation, K7t)
+    CUtensorMap tmap_fine;
+    bool tmap_ok;
     int64_t cap_cvis;
 
     // points
@@ -197,7 +202,7 @@ inline int64_t nk_sm_smem_bytes(int type, int dim, int prec, int w, const int *b
              3 * (3 * (kTileBatch + 2) * rs + kTileBatch * 2 * rs) + 32;   // + TMA ring
     else if (nk_interp_tiled(type, dim, prec, w, NK_SM, msub))
         // per warp (16): kernel rows [3][16][8] doubles; chunk starts
-        b += 16 * 3 * kTileWin * 8 * rs + 4 * (int64_t)(kTileMsub + 1);
+        b += 16 * 3 * kTileWin * 8 * rs + 4 * (int64_t)(kTileMsub + 4) + 16;
     else if (type == 1 && dim == 3)
         b += (int64_t)nk_sm3_batch(prec) *
              (((prec == NK_DOUBLE && w <= 16) ? 32 : w) * rs + 3 * w * rs + 16);

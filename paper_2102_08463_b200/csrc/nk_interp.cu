@@ -421,7 +421,7 @@ k_interp_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
                const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
                const double *__restrict__ pts, int64_t pitch,
                const double2 *__restrict__ fine, Geom g, double2 *__restrict__ out,
-               int64_t stage_off) {
+               int64_t stage_off, const __grid_constant__ CUtensorMap tmap, int use_tma) {
     constexpr int WIN = kTileWin, L = nk_tile_lg(W), TM = (1 << L) - 1, NWARP = 16;
     // staged rows: [3 axes][16 cells][8 points], point slot swizzled by cell
     // bit 1 (conflict-free B fragment and epilogue reads)
@@ -434,7 +434,8 @@ k_interp_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
     double *wst = reinterpret_cast<double *>(smem_raw + stage_off) +
                   (threadIdx.x >> 5) * (3 * WIN * CS);
     int *cstart = reinterpret_cast<int *>(smem_raw + stage_off) + 2 * NWARP * 3 * WIN * CS;
-    __shared__ int sh_nchunk;
+    int &sh_nchunk = cstart[kTileMsub + 1];
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(cstart + kTileMsub + 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x;
     fine += blockIdx.y * g.ntot;
@@ -446,8 +447,23 @@ k_interp_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
     const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
     const int p3 = min(g.m[2], g.n[2] - corner[2]) + 2 * h;
     const int pstride = p1 * p2;
-    stage_padded_bin<double, 3>(buf, fine, g, sub_bin[s]);
-    nk_cp_async_commit();
+    // the padded bin: one TMA box when it is full-size and does not wrap,
+    // else cp.async per cell with periodic wrap
+    const int o1 = corner[0] - h, o2 = corner[1] - h, o3 = corner[2] - h;
+    const bool tma = use_tma && p1 == g.m[0] + 2 * h && p2 == g.m[1] + 2 * h &&
+                     p3 == g.m[2] + 2 * h && o1 >= 0 && o2 >= 0 && o3 >= 0 &&
+                     o1 + p1 <= g.n[0] && o2 + p2 <= g.n[1] && o3 + p3 <= g.n[2];
+    if (tma) {
+        if (threadIdx.x == 0) {
+            nk_mbar_init(mbar, 1);
+            nk_fence_mbar_init();
+            nk_mbar_expect_tx(mbar, (unsigned)(p1 * p2 * p3) * 16u);
+            nk_tma_load_4d(buf, &tmap, 2 * o1, o2, o3, blockIdx.y, mbar);
+        }
+    } else {
+        stage_padded_bin<double, 3>(buf, fine, g, sub_bin[s]);
+        nk_cp_async_commit();
+    }
     const double half = 0.5 * W;
     const int j0 = sub_start[s], j1 = sub_stop[s];
     auto tile_of = [&](int j) {
@@ -481,7 +497,12 @@ k_interp_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
             sh_nchunk = nc;
         }
     }
-    nk_cp_async_wait<0>();
+    if (tma) {
+        __syncthreads();   // the mbarrier is initialised
+        nk_mbar_wait(mbar, 0);
+    } else {
+        nk_cp_async_wait<0>();
+    }
     __syncthreads();   // padded bin and chunk list ready
     const int nchunk = sh_nchunk;
     const int kx = lane & 3, prow = lane >> 2, ylane = lane >> 3, cpart = (lane >> 2) & 1;
@@ -584,10 +605,13 @@ int launch_w(nk_plan *p, const void *fine, void *out, int *launches) {
                 NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)one));
                 const int64_t stage_off = (p->max_pad_cells * 16 + 15) / 16 * 16;
+                // TMA box loads only from the plan's own grid (the tensor map
+                // describes p->d_fine); stage-level calls pass other grids
+                const int use_tma = p->tmap_ok && fine == p->d_fine && !getenv("NK_NO_TMA");
                 kern<<<dim3((unsigned)p->S, p->ntrans), 512, one, p->stream>>>(
                     p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm,
                     (const double *)p->d_pts, p->cap_M, (const double2 *)fine, p->geom,
-                    (double2 *)out, stage_off);
+                    (double2 *)out, stage_off, p->tmap_fine, use_tma);
                 NK_LAUNCH_CHECK();
                 ++*launches;
                 return NK_OK;

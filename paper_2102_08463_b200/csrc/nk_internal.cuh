@@ -112,6 +112,7 @@ struct nk_plan {
     int32_t *d_counts;      // nbins
     int32_t *d_starts;      // nbins + 1
     void *d_pts;            // dim arrays of cap_M local coords (plan precision)
+    void *d_rec;            // per input point (u1, u2[, u3, 0]) records (K1 -> K5)
     int32_t *d_alt_keys, *d_alt_vals;  // radix scratch
     int32_t *d_sort_scr;    // 4 cap_M int32: (bin, start) ordering scratch (type-1 SM)
     int32_t *d_tile_hist;

@@ -15,7 +15,7 @@
 namespace {
 
 constexpr int SORT_BLOCK = 256;
-constexpr int SORT_ITEMS = 8;
+constexpr int SORT_ITEMS = 16;
 constexpr int SORT_TILE = SORT_BLOCK * SORT_ITEMS;  // keys per tile
 constexpr int SORT_WARPS = SORT_BLOCK / 32;
 constexpr int RADIX_BITS = 8;
@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(256)
 k_fold_keys(int M, const TC *__restrict__ x, const TC *__restrict__ y,
             const TC *__restrict__ z, int64_t stride, Geom g, int32_t *__restrict__ keys,
             int32_t *__restrict__ counts, unsigned long long *__restrict__ bad,
-            int32_t *__restrict__ ckeys, int sb) {
+            int32_t *__restrict__ ckeys, int sb, T *__restrict__ rec) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     bool in = i < M;
     unsigned mask = __ballot_sync(0xffffffffu, in);
@@ -44,6 +44,7 @@ k_fold_keys(int M, const TC *__restrict__ x, const TC *__restrict__ y,
     const TC *ax[3] = {x, y, z};
     int key = 0, kstride = 1;
     int t[3] = {0, 0, 0}, pd[3] = {1, 1, 1};
+    T u[3] = {0, 0, 0};
     bool ok = true;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -55,12 +56,13 @@ k_fold_keys(int M, const TC *__restrict__ x, const TC *__restrict__ y,
             const int b = c / g.m[a];
             key += kstride * b;
             kstride *= g.nb[a];
+            // local coordinate in plan precision (K5: the visit-order
+            // gather copies these records) and, for SM plans, the footprint
+            // start in the bin's padded frame from the same value
+            const int corner = b * g.m[a];
+            u[a] = (T)(v - (double)corner);
             if (ckeys) {
-                // footprint start in the bin's padded frame, from the same
-                // plan-precision local coordinate the kernels use (K5)
-                const int corner = b * g.m[a];
-                const T u = (T)(v - (double)corner);
-                t[a] = (int)nk_ceil<T>(u - (T)(0.5 * g.w)) + g.halo;
+                t[a] = (int)nk_ceil<T>(u[a] - (T)(0.5 * g.w)) + g.halo;
                 pd[a] = min(g.m[a], g.n[a] - corner) + 2 * g.halo;
             }
         }
@@ -69,8 +71,24 @@ k_fold_keys(int M, const TC *__restrict__ x, const TC *__restrict__ y,
         atomicMin(bad, (unsigned long long)i);
         key = 0;
         t[0] = t[1] = t[2] = 0;
+        u[0] = u[1] = u[2] = 0;
     }
     keys[i] = key;
+    // record (u1, u2[, u3, 0]): one aligned 8/16/32-byte vector per point
+    if (g.dim == 3) {
+        if constexpr (sizeof(T) == 8) {
+            double2 *r = reinterpret_cast<double2 *>(rec) + 2 * (int64_t)i;
+            r[0] = make_double2(u[0], u[1]);
+            r[1] = make_double2(u[2], 0.0);
+        } else {
+            reinterpret_cast<float4 *>(rec)[i] = make_float4(u[0], u[1], u[2], 0.0f);
+        }
+    } else {
+        if constexpr (sizeof(T) == 8)
+            reinterpret_cast<double2 *>(rec)[i] = make_double2(u[0], u[1]);
+        else
+            reinterpret_cast<float2 *>(rec)[i] = make_float2(u[0], u[1]);
+    }
     if (ckeys)
         ckeys[i] = (int32_t)(((unsigned)key << sb) |
                              (unsigned)nk_start_code(t[0], t[1], t[2], pd[0], pd[1], g));
@@ -256,11 +274,19 @@ __global__ void __launch_bounds__(SORT_BLOCK)
 k_radix_scatter(const int32_t *__restrict__ keys_in, const int32_t *__restrict__ vals_in,
                 int M, int shift, int ntiles, const int32_t *__restrict__ offs,
                 int32_t *__restrict__ keys_out, int32_t *__restrict__ vals_out) {
+    // 1) stable ranks inside each warp's slice (8 ballots per item, per-warp
+    //    digit counters); 2) the tile is reordered by digit in shared memory;
+    //    3) written out in that order, so consecutive threads store
+    //    consecutive slots of each digit's run (coalesced; a 4096-key tile
+    //    gives runs of ~16 keys per digit instead of scattered words)
     __shared__ int wcnt[SORT_WARPS][RADIX];
+    __shared__ int lstart[RADIX], gstart[RADIX];
+    __shared__ int skey[SORT_TILE], sval[SORT_TILE];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < SORT_WARPS * RADIX; i += blockDim.x) (&wcnt[0][0])[i] = 0;
     __syncthreads();
-    const int base = blockIdx.x * SORT_TILE + warp * 32 * SORT_ITEMS;
+    const int tbase = blockIdx.x * SORT_TILE;
+    const int base = tbase + warp * 32 * SORT_ITEMS;
     const unsigned lt = (1u << lane) - 1u;
     int key[SORT_ITEMS], val[SORT_ITEMS], rank[SORT_ITEMS];
 #pragma unroll
@@ -270,8 +296,6 @@ k_radix_scatter(const int32_t *__restrict__ keys_in, const int32_t *__restrict__
         key[it] = valid ? keys_in[idx] : 0;
         val[it] = valid ? (vals_in ? vals_in[idx] : idx) : 0;
         const int d = (key[it] >> shift) & (RADIX - 1);
-        // lanes with the same digit: 8 ballots (ALU) instead of match.any
-        // (ADU-pipe bound: 43 % busy, 10 % issue)
         unsigned peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
         for (int b = 0; b < RADIX_BITS; ++b) {
@@ -282,28 +306,43 @@ k_radix_scatter(const int32_t *__restrict__ keys_in, const int32_t *__restrict__
         __syncwarp();
         if (valid && lane == __ffs(peers) - 1) wcnt[warp][d] = c + __popc(peers);
         __syncwarp();
-        rank[it] = c + __popc(peers & lt);
+        rank[it] = valid ? c + __popc(peers & lt) : -1;
     }
     __syncthreads();
+    // digit d (thread d): per-warp exclusive offsets inside the digit, the
+    // digit's tile total, its global start (scanned upsweep histogram)
+    int tot = 0;
     for (int d = threadIdx.x; d < RADIX; d += blockDim.x) {
-        int run = offs[(int64_t)d * ntiles + blockIdx.x];
 #pragma unroll
         for (int w = 0; w < SORT_WARPS; ++w) {
-            int c = wcnt[w][d];
-            wcnt[w][d] = run;
-            run += c;
+            const int cnt = wcnt[w][d];
+            wcnt[w][d] = tot;
+            tot += cnt;
         }
+        gstart[d] = offs[(int64_t)d * ntiles + blockIdx.x];
     }
+    int tile_tot;
+    static_assert(RADIX == SORT_BLOCK, "one digit per thread");
+    const int ex = block_excl_scan(tot, &tile_tot);
+    lstart[threadIdx.x] = ex;
     __syncthreads();
 #pragma unroll
     for (int it = 0; it < SORT_ITEMS; ++it) {
-        int idx = base + it * 32 + lane;
-        if (idx < M) {
-            int d = (key[it] >> shift) & (RADIX - 1);
-            int pos = wcnt[warp][d] + rank[it];
-            keys_out[pos] = key[it];
-            vals_out[pos] = val[it];
+        if (rank[it] >= 0) {
+            const int d = (key[it] >> shift) & (RADIX - 1);
+            const int lp = lstart[d] + wcnt[warp][d] + rank[it];
+            skey[lp] = key[it];
+            sval[lp] = val[it];
         }
+    }
+    __syncthreads();
+    const int n = min(SORT_TILE, M - tbase);
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        const int k = skey[t];
+        const int d = (k >> shift) & (RADIX - 1);
+        const int pos = gstart[d] + (t - lstart[d]);
+        keys_out[pos] = k;
+        vals_out[pos] = sval[t];
     }
 }
 
@@ -353,24 +392,36 @@ __global__ void k_export_subs(int S, Geom g, const int32_t *__restrict__ sub_bin
 // ---------------------------------------------------------------- K5
 // Visit-order local coordinates u = v - bin corner, in plan precision
 // (a float keeps ~4e-6 cell resolution inside a 32-cell bin where a float
-// global v would lose 1e-4 cells at n = 2048).
-template <typename TC, typename T>
+// global v would lose 1e-4 cells at n = 2048).  K1 wrote each point's
+// coordinates as one aligned record in input order; this gathers the
+// records through the visit permutation (one sector per point instead of
+// one per coordinate) and writes them as SoA rows.
+template <typename T, int D>
 __global__ void __launch_bounds__(256)
-k_gather_points(int M, const int32_t *__restrict__ perm, const TC *__restrict__ x,
-                const TC *__restrict__ y, const TC *__restrict__ z, int64_t stride, Geom g,
+k_gather_points(int M, const int32_t *__restrict__ perm, const T *__restrict__ rec,
                 T *__restrict__ pts, int64_t pitch) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= M) return;
-    int i = perm ? perm[j] : j;
-    const TC *ax[3] = {x, y, z};
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        if (a < g.dim) {
-            double v = nk_fold((double)ax[a][(int64_t)i * stride], g.scale[a]);
-            int c = nk_cell(v, g.n[a]);
-            int corner = (c / g.m[a]) * g.m[a];
-            pts[a * pitch + j] = (T)(v - (double)corner);
-        }
+    const int64_t i = perm ? perm[j] : j;
+    if constexpr (D == 3 && sizeof(T) == 8) {
+        const double2 a = __ldg(reinterpret_cast<const double2 *>(rec) + 2 * i);
+        const double b = __ldg(rec + 4 * i + 2);
+        pts[j] = a.x;
+        pts[pitch + j] = a.y;
+        pts[2 * pitch + j] = b;
+    } else if constexpr (D == 3) {
+        const float4 a = __ldg(reinterpret_cast<const float4 *>(rec) + i);
+        pts[j] = a.x;
+        pts[pitch + j] = a.y;
+        pts[2 * pitch + j] = a.z;
+    } else if constexpr (sizeof(T) == 8) {
+        const double2 a = __ldg(reinterpret_cast<const double2 *>(rec) + i);
+        pts[j] = a.x;
+        pts[pitch + j] = a.y;
+    } else {
+        const float2 a = __ldg(reinterpret_cast<const float2 *>(rec) + i);
+        pts[j] = a.x;
+        pts[pitch + j] = a.y;
     }
 }
 
@@ -534,7 +585,8 @@ static int ensure_point_buffers(nk_plan *p, int64_t M) {
     if (M <= p->cap_M && p->d_keys) return NK_OK;
     void **bufs[] = {(void **)&p->d_keys_in, (void **)&p->d_keys, (void **)&p->d_perm,
                      (void **)&p->d_alt_keys, (void **)&p->d_alt_vals, &p->d_pts,
-                     (void **)&p->d_vperm_buf, &p->d_pts_alt, (void **)&p->d_sort_scr};
+                     (void **)&p->d_vperm_buf, &p->d_pts_alt, (void **)&p->d_sort_scr,
+                     &p->d_rec};
     for (void **b : bufs) {
         if (*b) cudaFree(*b);
         *b = nullptr;
@@ -548,6 +600,7 @@ static int ensure_point_buffers(nk_plan *p, int64_t M) {
     NK_CUDA(cudaMalloc((void **)&p->d_alt_keys, 4 * n));
     NK_CUDA(cudaMalloc((void **)&p->d_alt_vals, 4 * n));
     NK_CUDA(cudaMalloc(&p->d_pts, (size_t)p->csize / 2 * p->dim * n));
+    NK_CUDA(cudaMalloc(&p->d_rec, (size_t)p->csize / 2 * (p->dim == 3 ? 4 : 2) * n));
     if (p->method == NK_SM)
         NK_CUDA(cudaMalloc((void **)&p->d_sort_scr, 4 * 4 * n));
     if (p->method == NK_SM) {
@@ -565,22 +618,24 @@ static int fold_keys(nk_plan *p, const void *x, const void *y, const void *z, in
     if (p->prec == NK_DOUBLE)
         k_fold_keys<TC, double><<<blocks_for(M, 256), 256, 0, p->stream>>>(
             M, (const TC *)x, (const TC *)y, (const TC *)z, stride, p->geom, p->d_keys_in,
-            p->method == NK_GM ? p->d_counts : nullptr, p->d_bad, ckeys, sb);
+            p->method == NK_GM ? p->d_counts : nullptr, p->d_bad, ckeys, sb, (double *)p->d_rec);
     else
         k_fold_keys<TC, float><<<blocks_for(M, 256), 256, 0, p->stream>>>(
             M, (const TC *)x, (const TC *)y, (const TC *)z, stride, p->geom, p->d_keys_in,
-            p->method == NK_GM ? p->d_counts : nullptr, p->d_bad, ckeys, sb);
+            p->method == NK_GM ? p->d_counts : nullptr, p->d_bad, ckeys, sb, (float *)p->d_rec);
     NK_LAUNCH_CHECK();
     return NK_OK;
 }
 
-template <typename TC, typename T>
-static int gather(nk_plan *p, const int32_t *perm, const void *x, const void *y, const void *z,
-                  int64_t stride) {
+template <typename T>
+static int gather(nk_plan *p, const int32_t *perm) {
     int M = (int)p->M;
-    k_gather_points<TC, T><<<blocks_for(M, 256), 256, 0, p->stream>>>(
-        M, perm, (const TC *)x, (const TC *)y, (const TC *)z, stride, p->geom, (T *)p->d_pts,
-        p->cap_M);
+    if (p->dim == 3)
+        k_gather_points<T, 3><<<blocks_for(M, 256), 256, 0, p->stream>>>(
+            M, perm, (const T *)p->d_rec, (T *)p->d_pts, p->cap_M);
+    else
+        k_gather_points<T, 2><<<blocks_for(M, 256), 256, 0, p->stream>>>(
+            M, perm, (const T *)p->d_rec, (T *)p->d_pts, p->cap_M);
     NK_LAUNCH_CHECK();
     return NK_OK;
 }
@@ -722,12 +777,7 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
         NK_CUDA(cudaMemcpyAsync(p->d_keys, p->d_keys_in, 4 * M, cudaMemcpyDeviceToDevice, st));
     }
     if (M > 0) {
-        if (p->prec == NK_DOUBLE)
-            rc = coord_prec == NK_DOUBLE ? gather<double, double>(p, perm, x, y, z, stride)
-                                         : gather<float, double>(p, perm, x, y, z, stride);
-        else
-            rc = coord_prec == NK_DOUBLE ? gather<double, float>(p, perm, x, y, z, stride)
-                                         : gather<float, float>(p, perm, x, y, z, stride);
+        rc = p->prec == NK_DOUBLE ? gather<double>(p, perm) : gather<float>(p, perm);
         if (rc) return rc;
     }
 

@@ -150,6 +150,7 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     // add the register sums of the window to its planes, then clear
     // (lanes outside the footprint / window never write)
     auto flush = [&]() {
+        __syncwarp();   // lanes' cells moved with the window: order the accesses
 #pragma unroll
         for (int k = 0; k < NE; ++k) {
             const int e = e0 + k * NW;
@@ -557,6 +558,9 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
         // carry zero sums (footprints lie inside)
         // (all 8 loads first: the lane's cells are distinct, so no store can
         // alias a later load, which the compiler cannot prove)
+        // (the window moved since the warp's last flush: a cell another lane
+        // wrote then may be this lane's now -- order the warp's accesses)
+        __syncwarp();
         const int zpl = a3 + e;
         if (zpl < p3 && !(dbg & 2)) {
             double2 *pl = buf + zpl * pstride + (a2 + kp) * p1 + a1 + row;
@@ -652,6 +656,7 @@ k_spread_sm2(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     int run = -1;
     auto flush = [&]() {
         if (run < 0) return;
+        __syncwarp();   // lanes' cells moved with the run start: order the accesses
 #pragma unroll
         for (int it = 0; it < NIT; ++it) {
             if (it < NIT - 1 || last_ok) {

@@ -72,3 +72,79 @@ def test_sharded_plan_nccl_world1(env, orc):
             assert orc.rel_l2_error(got, ref) < 1e-6
     finally:
         dist.destroy_process_group()
+
+
+def _gpu_worker(rank, world, port, outdir, cfg):
+    """One rank of the 2-process CUDA test: this rank's point shard through
+    ShardedPlan(CudaStageOps) on cuda:0 (both ranks share the one GPU; gloo
+    carries the CUDA-tensor all-reduce / broadcast)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    import paper_2102_08463_b200 as nk
+    from paper_2102_08463_b200 import dist as nkd
+    from oracle import oracle as orc
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        modes, eps, prec, M = cfg
+        grid = orc.make_grid(modes, eps, prec)
+        rdt = np.float32 if prec == "single" else np.float64
+        cdt = np.complex64 if prec == "single" else np.complex128
+        pts = orc.gen_points("rand", M, grid, 8, rdt)
+        c = torch.from_numpy(orc.gen_strengths(M, 8, cdt)).cuda()
+        f = torch.from_numpy(orc.gen_strengths(int(np.prod(modes)), 9, cdt)
+                             .reshape(modes[::-1])).cuda()
+        lo, hi = nkd.shard_bounds(M, world, rank)
+        res = {}
+        p1 = nk.make_plan(1, modes, eps, precision=prec)
+        p1.set_points(pts[lo:hi])
+        res["t1"] = nkd.ShardedPlan(nkd.CudaStageOps(p1), 1, all_ranks=True).execute(
+            c[lo:hi].contiguous()).cpu().numpy()
+        p2 = nk.make_plan(2, modes, eps, precision=prec)
+        p2.set_points(pts[lo:hi])
+        fin = f if rank == 0 else torch.zeros_like(f)
+        res["t2"] = nkd.ShardedPlan(nkd.CudaStageOps(p2), 2, root=0).execute(fin).cpu().numpy()
+        np.savez(os.path.join(outdir, f"rank{rank}.npz"), lo=lo, hi=hi, **res)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg", [((40, 44), 1e-6, "single", 30001),
+                                 ((16, 20, 12), 1e-12, "double", 20001)])
+def test_sharded_plan_two_processes_cuda(env, orc, cfg):
+    """World-size-2 ShardedPlan over the CUDA stage ops (two processes on
+    one GPU, gloo): type 1 (per-rank spread + all-reduce of the fine grids +
+    FFT / deconvolution) and type 2 (root's modes broadcast, per-rank
+    interpolation) must equal the unsharded plan."""
+    import tempfile
+    import torch.multiprocessing as mp
+    torch, nk, nkd = env
+    modes, eps, prec, M = cfg
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_gpu_worker, args=(2, port, d, cfg), nprocs=2, join=True)
+        outs = [np.load(os.path.join(d, f"rank{r}.npz")) for r in range(2)]
+    grid = orc.make_grid(modes, eps, prec)
+    rdt = np.float32 if prec == "single" else np.float64
+    cdt = np.complex64 if prec == "single" else np.complex128
+    pts = orc.gen_points("rand", M, grid, 8, rdt)
+    c = torch.from_numpy(orc.gen_strengths(M, 8, cdt)).cuda()
+    f = torch.from_numpy(orc.gen_strengths(int(np.prod(modes)), 9, cdt).reshape(modes[::-1])).cuda()
+    p1 = nk.make_plan(1, modes, eps, precision=prec)
+    p1.set_points(pts)
+    ref1 = p1.execute(c).cpu().numpy()
+    p2 = nk.make_plan(2, modes, eps, precision=prec)
+    p2.set_points(pts)
+    ref2 = p2.execute(f).cpu().numpy()
+    tol = 1e-5 if prec == "single" else 1e-12
+    for o in outs:
+        assert orc.rel_l2_error(o["t1"], ref1) < tol
+        lo, hi = int(o["lo"]), int(o["hi"])
+        assert orc.rel_l2_error(o["t2"], ref2[lo:hi]) < tol
+    assert int(outs[0]["hi"]) == int(outs[1]["lo"]) and int(outs[1]["hi"]) == M

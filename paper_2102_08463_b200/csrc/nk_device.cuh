@@ -279,9 +279,17 @@ __device__ __forceinline__ void nk_red(double2 *p, double re, double im) {
 // for tiled plans tile-major -- all starts of one 2^L x 2^L x 2^L tile are
 // adjacent, so the tiled f64 spread (K6t) accumulates them in one register
 // window.
+// Tiles start at the smallest footprint start, t0 = halo - floor(w / 2)
+// (u >= 0 in the bin): a bin of m cells has starts t0 .. t0 + m, so bins
+// with m + 1 a multiple of the tile size are covered by whole tiles.
+__device__ __forceinline__ int nk_tile_t0(const Geom &g) { return g.halo - g.w / 2; }
 __device__ __forceinline__ int nk_start_code(int t1, int t2, int t3, int p1, int p2,
                                              const Geom &g) {
     if (!g.tiled) return (t3 * p2 + t2) * p1 + t1;
+    const int o = nk_tile_t0(g);
+    t1 -= o;
+    t2 -= o;
+    t3 -= o;
     const int L = g.tile_lg, m = (1 << L) - 1;
     const int nt1 = (p1 + m) >> L, nt2 = (p2 + m) >> L;
     const int tile = ((t3 >> L) * nt2 + (t2 >> L)) * nt1 + (t1 >> L);

@@ -515,13 +515,13 @@ k_interp_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
             const int q = lane / 3, ax = lane - 3 * q;
             double k[W];
             const int t = nk_kernel_row_poly<W>(__ldg(pts + ax * pitch + cs + q), g, k) + h;
-            const int sh = t & TM;
+            const int sh = (t - nk_tile_t0(g)) & TM;
             double *dst = wst + ax * WIN * CS;
 #pragma unroll
             for (int i = 0; i < WIN - W; ++i) dst[pos(i < sh ? i : i + W, q)] = 0.0;
 #pragma unroll
             for (int r = 0; r < W; ++r) dst[pos(sh + r, q)] = k[r];
-            t0 = t & ~TM;
+            t0 = nk_tile_t0(g) + ((t - nk_tile_t0(g)) & ~TM);
         }
         // the chunk's window anchor (any point's tile corner: lanes 0-2)
         const int a1 = __shfl_sync(0xffffffffu, t0, 0);

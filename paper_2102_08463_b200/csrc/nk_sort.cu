@@ -302,10 +302,14 @@ k_radix_scatter(const int32_t *__restrict__ keys_in, const int32_t *__restrict__
             const unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1);
             peers &= ((d >> b) & 1) ? bb : ~bb;
         }
-        int c = valid ? wcnt[warp][d] : 0;
-        __syncwarp();
-        if (valid && lane == __ffs(peers) - 1) wcnt[warp][d] = c + __popc(peers);
-        __syncwarp();
+        // the digit group's leader bumps the warp's counter (native shared
+        // integer atomic; a warp's atomics land in program order, so ranks
+        // stay stable) and broadcasts the old value -- no read / write
+        // round trip through shared memory between consecutive items
+        const int leader = __ffs(peers) - 1;
+        int c = 0;
+        if (valid && lane == leader) c = atomicAdd(&wcnt[warp][d], __popc(peers));
+        c = __shfl_sync(0xffffffffu, c, valid ? leader : lane);
         rank[it] = valid ? c + __popc(peers & lt) : -1;
     }
     __syncthreads();

@@ -397,7 +397,7 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
             const double u = ru[ax * RU + q];
             const double st = ceil(u - half);
             const int t = (int)st + h;
-            const int sh = t & TM;
+            const int sh = (t - nk_tile_t0(g)) & TM;
             const double d = st - u;
             const double z0 = d * (2.0 / W), sp = fma(2.0, d, (double)(W - 1));
             double2 cv = make_double2(0.0, 0.0);
@@ -430,9 +430,12 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
             if (part == 0 && ax == 0) {
                 const double u2 = ru[RU + q], u3 = ru[2 * RU + q];
                 const int t2 = (int)ceil(u2 - half) + h, t3 = (int)ceil(u3 - half) + h;
+                // tile corner (window anchor) per axis, t3's offset in its tile
+                const int o = nk_tile_t0(g);
                 sinfo[q] = make_int4(nk_start_code(t, t2, t3, p1, p2, g) >> (3 * L),
-                                     (t & ~TM) | ((t2 & ~TM) << 8) | ((t3 & ~TM) << 16),
-                                     t3 & TM, 0);
+                                     (o + ((t - o) & ~TM)) | ((o + ((t2 - o) & ~TM)) << 8) |
+                                         ((o + ((t3 - o) & ~TM)) << 16),
+                                     (t3 - o) & TM, 0);
             }
         }
     };

@@ -320,7 +320,7 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     if (tiled) {
         p->start_space = (int64_t)1 << (3 * tlg);
         for (int i = 0; i < dim; ++i)
-            p->start_space *= (p->bin_dims[i] + 2 * p->halo + (1 << tlg) - 1) >> tlg;
+            p->start_space *= (p->bin_dims[i] + 1 + (1 << tlg) - 1) >> tlg;
     }
 
     // geometry for kernels

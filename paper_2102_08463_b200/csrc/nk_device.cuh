@@ -290,8 +290,9 @@ __device__ __forceinline__ int nk_start_code(int t1, int t2, int t3, int p1, int
     t1 -= o;
     t2 -= o;
     t3 -= o;
+    // starts t - t0 lie in [0, bin width] (p - 2 halo + 1 values per axis)
     const int L = g.tile_lg, m = (1 << L) - 1;
-    const int nt1 = (p1 + m) >> L, nt2 = (p2 + m) >> L;
+    const int nt1 = (p1 - 2 * g.halo + 1 + m) >> L, nt2 = (p2 - 2 * g.halo + 1 + m) >> L;
     const int tile = ((t3 >> L) * nt2 + (t2 >> L)) * nt1 + (t1 >> L);
     return (tile << (3 * L)) | ((((t3 & m) << L) | (t2 & m)) << L) | (t1 & m);
 }

@@ -83,22 +83,45 @@ def _type2_direct_check(nk, orc, plan, pts, modes, f, n_pts=64, seed=2):
 # ---------------------------------------------------------------- C4
 
 @pytest.mark.parametrize("nufft_type", [1, 2])
-def test_c4_geometry_sort_32bit_key(nk, orc, nufft_type):
-    """C4 (N=256^3, n=512^3, eps 1e-12, f64) with the default tuned bins:
-    2^18 bins x 2^14 padded-bin start cells, so the composite (bin, start)
-    sort key uses all 32 bits (sign bit included).  1.5e6 uniform points;
-    the exported layout must equal binsort.py's bit for bit."""
+def test_c4_geometry_sort(nk, orc, nufft_type):
+    """C4 (N=256^3, n=512^3, eps 1e-12, f64) with the default tuned bins and
+    the tile-major start order of the tiled spread / interp.  1.5e6 uniform
+    points; the exported layout must equal binsort.py's bit for bit."""
     modes, eps, M = (256, 256, 256), 1e-12, 1_500_001   # odd M on purpose
     grid = orc.make_grid(modes, eps, "double")
     pts = orc.gen_points("rand", M, grid, 40 + nufft_type)
     p = nk.make_plan(nufft_type, modes, eps, "sm", "double")
-    if nufft_type == 2:   # (type 1 sorts by start block: fewer bits, K6g)
-        nb = int(np.prod([(n + m - 1) // m for n, m in zip(p.grid.fine, p.bin_dims)]))
-        cells = int(np.prod([m + 2 * p.params.halo for m in p.bin_dims]))
-        assert (nb - 1).bit_length() + (cells - 1).bit_length() == 32
     p.set_points(pts)
     _sorted_layout_matches(nk, orc, p, pts, modes)
     p.destroy()
+
+
+@pytest.mark.parametrize("nufft_type", [1, 2])
+def test_composite_key_uses_32_bits(nk, orc, nufft_type):
+    """N=256^3 (n=512^3) single precision, eps 1e-6, bins 4 x 4 x 4: 2^21
+    bins x 12^3 padded-bin start cells, so the composite (bin, start) sort
+    key uses all 32 bits (sign bit included).  The exported layout must
+    equal binsort.py's bit for bit and the transform the GM-sort plan's."""
+    modes, eps, M = (256, 256, 256), 1e-6, 1_000_001
+    grid = orc.make_grid(modes, eps, "single")
+    pts = orc.gen_points("rand", M, grid, 50 + nufft_type, np.float32)
+    p = nk.make_plan(nufft_type, modes, eps, "sm", "single", bin_dims=(4, 4, 4))
+    nb = int(np.prod([(n + m - 1) // m for n, m in zip(p.grid.fine, p.bin_dims)]))
+    cells = int(np.prod([m + 2 * p.params.halo for m in p.bin_dims]))
+    assert (nb - 1).bit_length() + (cells - 1).bit_length() == 32
+    p.set_points(pts)
+    _sorted_layout_matches(nk, orc, p, pts, modes)
+    q = nk.make_plan(nufft_type, modes, eps, "gmsort", "single")
+    q.set_points(pts)
+    rng = np.random.default_rng(nufft_type)
+    if nufft_type == 1:
+        inp = orc.gen_strengths(M, 3).astype(np.complex64)
+    else:
+        inp = (rng.standard_normal(modes[::-1]) + 1j * rng.standard_normal(modes[::-1])
+               ).astype(np.complex64)
+    assert orc.rel_l2_error(p.execute(inp), q.execute(inp)) < 1e-5
+    p.destroy()
+    q.destroy()
 
 
 def test_c4_geometry_transforms(nk, orc):

@@ -122,6 +122,23 @@ def fp64_peak():
         return 148 * 64 * 2 * 1.965e9 / 1e12, "architectural: 148 SMs x 64 DFMA/clk x 2 x 1965 MHz"
 
 
+def dmma_peak():
+    """Measured FP64 tensor-core (DMMA m8n8k4) throughput in TFLOP/s, the
+    best of profiles/r2/dmma_peak.json (scripts/dmma_peak.cu), else the
+    FP64 FMA peak (B200 runs both at the same rate)."""
+    try:
+        best = 0.0
+        with open(os.path.join(ROOT, "profiles", "r2", "dmma_peak.json")) as fh:
+            for ln in fh:
+                j = json.loads(ln)
+                best = max(best, float(j.get("dmma_tflops", 0.0)))
+        if best > 0:
+            return best, "measured (profiles/r2/dmma_peak.json, scripts/dmma_peak.cu)"
+    except Exception:
+        pass
+    return fp64_peak()
+
+
 class Clocks:
     """nvidia-smi sampler during the timed region (B200_PROFILING.md)."""
 
@@ -639,6 +656,28 @@ def run_ours(args, cfg):
                                 "algorithmic_bytes": B, "kernel_ms": dom_ms,
                                 "kernel_ms_by_type": {f"type{t}": v for t, v in kern_avg.items()},
                                 "peak_source": peak_src}
+            if cfg["prec"] == "double" and d == 3 and w >= 9 and \
+                    plans[dom_type].method == "sm":
+                # the tiled f64 spread / interp (K6t / K7t) run on the FP64
+                # tensor cores: algorithmic flops = 4 w^3 per point (w^3
+                # complex x real FMAs) over the measured DMMA peak; the
+                # issued DMMA flops cover the 16^3 tile window (4 * 16^3)
+                tpk, tpk_src = dmma_peak()
+                flops = 4.0 * M * w ** d
+                ach_t = flops / (dom_ms / 1e3) / 1e12
+                hbm = line["roofline"]
+                line["roofline"] = {"bound": "tensor",
+                                    "kernel": hbm["kernel"] + " (DMMA m8n8k4)",
+                                    "achieved": ach_t, "peak": tpk, "unit": "TFLOP/s",
+                                    "frac": ach_t / tpk, "traffic": hbm["traffic"],
+                                    "algorithmic_flops": flops,
+                                    "issued_flops": 4.0 * M * 16 ** 3,
+                                    "kernel_ms": dom_ms,
+                                    "kernel_ms_by_type": hbm["kernel_ms_by_type"],
+                                    "peak_source": tpk_src}
+                line["hbm_roofline"] = {k: hbm[k] for k in ("bound", "achieved", "peak", "unit",
+                                                            "frac", "algorithmic_bytes",
+                                                            "peak_source")}
             if cfg["prec"] == "double":
                 # the f64 spread / interp are FP64-pipe bound: w^d cell updates
                 # per point, each a complex x real FMA (2 DFMA = 4 flops)

@@ -65,12 +65,13 @@ typedef struct {
     int bin_dims[3];     /* 0 = default.  GM-sort plans: the reference's (32,32) /
                             (16,16,2) (binsort.py:34-35).  SM plans: B200-tuned shapes
                             -- type 1: 2D (16,8), 3D f32 (4,4,4), 3D f64 (16,8,4);
-                            type 2: 2D (32,32), 3D f32 (16,16,4), 3D f64 (8,8,8);
+                            type 2: 2D (32,32), 3D f32 (16,16,4), 3D f64 (7,7,7);
                             halved along axes 1/2 while the padded bin exceeds
                             shared memory */
     int max_subproblem;  /* 0 = default.  The reference default is 1024
                             (binsort.py:38); SM plans use 128 for 2D type 1, 1024
-                            for 3D type 1 and 4096 for type 2 */
+                            for 3D type 1 and 3D double type 2, 4096 for other
+                            type 2 */
     int64_t fine[3];     /* 0 = sizing rule n_i = next_smooth(max(2N_i, 2w)) */
     int device;          /* -1 = current device.  Every call on the plan runs on this
                             device and restores the caller's current device */

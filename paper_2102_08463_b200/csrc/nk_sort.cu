@@ -289,12 +289,18 @@ k_radix_scatter(const int32_t *__restrict__ keys_in, const int32_t *__restrict__
     const int base = tbase + warp * 32 * SORT_ITEMS;
     const unsigned lt = (1u << lane) - 1u;
     int key[SORT_ITEMS], val[SORT_ITEMS], rank[SORT_ITEMS];
+    // all of the warp's loads in flight before the ranking (the ranking's
+    // ballots / shuffles would otherwise wait on each load in turn)
+#pragma unroll
+    for (int it = 0; it < SORT_ITEMS; ++it) {
+        const int idx = base + it * 32 + lane;
+        key[it] = idx < M ? __ldcs(keys_in + idx) : 0;
+        val[it] = idx < M ? (vals_in ? __ldcs(vals_in + idx) : idx) : 0;
+    }
 #pragma unroll
     for (int it = 0; it < SORT_ITEMS; ++it) {
         int idx = base + it * 32 + lane;
         bool valid = idx < M;
-        key[it] = valid ? keys_in[idx] : 0;
-        val[it] = valid ? (vals_in ? vals_in[idx] : idx) : 0;
         const int d = (key[it] >> shift) & (RADIX - 1);
         unsigned peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll

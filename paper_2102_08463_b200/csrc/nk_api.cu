@@ -66,7 +66,7 @@ void free_plan(nk_plan *p) {
                     p->d_starts, p->d_pts, p->d_alt_keys, p->d_alt_vals, p->d_tile_hist,
                     p->d_scan_tmp, p->d_bad, p->d_nsub_off, p->d_sub_bin, p->d_sub_start,
                     p->d_sub_stop, p->d_in_stage, p->d_out_stage, p->d_vperm_buf,
-                    p->d_pts_alt, p->d_sort_scr, p->d_work, p->d_cvis, p->d_rec};
+                    p->d_pts_alt, p->d_sort_scr, p->d_work, p->d_cvis, p->d_rec, p->d_sub_sched};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p->fft_ok) cufftDestroy(p->fft);

@@ -127,6 +127,8 @@ struct nk_plan {
     int64_t S, cap_S;
     int32_t *d_nsub_off;    // nbins + 1
     int32_t *d_sub_bin, *d_sub_start, *d_sub_stop;
+    int32_t *d_sub_sched;   // tiled f64 kernels: CTA -> subproblem in Morton order of bins
+    int64_t cap_sched;
     int max_sub_smem;       // bytes of dynamic smem for the SM kernels
     int64_t max_pad_cells;  // prod(m_i + 2 halo)
     int64_t start_space;    // footprint-start codes per bin (nk_start_code range)

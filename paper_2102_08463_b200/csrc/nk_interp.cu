@@ -421,7 +421,8 @@ k_interp_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
                const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
                const double *__restrict__ pts, int64_t pitch,
                const double2 *__restrict__ fine, Geom g, double2 *__restrict__ out,
-               int64_t stage_off, const __grid_constant__ CUtensorMap tmap, int use_tma) {
+               int64_t stage_off, const __grid_constant__ CUtensorMap tmap, int use_tma,
+               const int32_t *__restrict__ sched) {
     constexpr int WIN = kTileWin, L = nk_tile_lg(W), TM = (1 << L) - 1, NWARP = 16;
     // staged rows: [3 axes][16 cells][8 points], point slot swizzled by cell
     // bit 1 (conflict-free B fragment and epilogue reads)
@@ -437,7 +438,7 @@ k_interp_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
     int &sh_nchunk = cstart[kTileMsub + 1];
     uint64_t *mbar = reinterpret_cast<uint64_t *>(cstart + kTileMsub + 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int s = blockIdx.x;
+    const int s = sched ? sched[blockIdx.x] : (int)blockIdx.x;
     fine += blockIdx.y * g.ntot;
     out += blockIdx.y * g.M;
     int corner[3];
@@ -611,7 +612,7 @@ int launch_w(nk_plan *p, const void *fine, void *out, int *launches) {
                 kern<<<dim3((unsigned)p->S, p->ntrans), 512, one, p->stream>>>(
                     p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm,
                     (const double *)p->d_pts, p->cap_M, (const double2 *)fine, p->geom,
-                    (double2 *)out, stage_off, p->tmap_fine, use_tma);
+                    (double2 *)out, stage_off, p->tmap_fine, use_tma, p->d_sub_sched);
                 NK_LAUNCH_CHECK();
                 ++*launches;
                 return NK_OK;

@@ -399,6 +399,30 @@ __global__ void k_export_subs(int S, Geom g, const int32_t *__restrict__ sub_bin
     }
 }
 
+// ---------------------------------------------------------------- K4m
+// Subproblem schedule of the tiled f64 kernels: Morton (Z-order) key of the
+// bin, so the CTAs in flight cover a compact block of bins and the halo
+// reductions (spread) / halo re-reads (interp) of neighbouring bins hit L2
+// (the bin-major order walks a whole 512^2 x halo slab between z-neighbours).
+__device__ __forceinline__ unsigned nk_spread_bits3(unsigned v) {   // 10 bits -> every 3rd
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000ffu;
+    v = (v | (v << 8)) & 0x0300f00fu;
+    v = (v | (v << 4)) & 0x030c30c3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+__global__ void k_sched_keys(int S, const int32_t *__restrict__ sub_bin, Geom g,
+                             int32_t *__restrict__ keys) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    const int b = sub_bin[s];
+    const int bx = b % g.nb[0], r = b / g.nb[0];
+    const int by = r % g.nb[1], bz = r / g.nb[1];
+    keys[s] = (int32_t)(nk_spread_bits3(bx) | (nk_spread_bits3(by) << 1) |
+                        (nk_spread_bits3(bz) << 2));
+}
+
 // ---------------------------------------------------------------- K5
 // Visit-order local coordinates u = v - bin corner, in plan precision
 // (a float keeps ~4e-6 cell resolution inside a 32-cell bin where a float
@@ -898,6 +922,28 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
                 p->d_vperm = vout;
             }
         }
+    }
+    // Morton schedule of the subproblems for the tiled f64 kernels (bins
+    // per axis <= 1024; the scratch is free once the visit order is set)
+    if (p->geom.tiled && p->S > 0 && p->dim == 3 && p->nb[0] <= 1024 && p->nb[1] <= 1024 &&
+        p->nb[2] <= 1024 && !getenv("NK_NO_SCHED")) {
+        if (p->S > p->cap_sched || !p->d_sub_sched) {
+            cudaFree(p->d_sub_sched);
+            p->d_sub_sched = nullptr;
+            NK_CUDA(cudaMalloc((void **)&p->d_sub_sched, 4 * (size_t)p->S));
+            p->cap_sched = p->S;
+        }
+        const int64_t q = p->cap_M;
+        int32_t *scr = p->d_sort_scr;
+        k_sched_keys<<<blocks_for(p->S, 256), 256, 0, st>>>((int)p->S, p->d_sub_bin, p->geom, scr);
+        NK_LAUNCH_CHECK();
+        rc = radix_sort_pairs(p, scr, nullptr, p->S, 30, scr + q, p->d_sub_sched, scr + 2 * q,
+                              scr + 3 * q);
+        if (rc) return rc;
+    } else if (p->d_sub_sched) {
+        cudaFree(p->d_sub_sched);
+        p->d_sub_sched = nullptr;
+        p->cap_sched = 0;
     }
     NK_CUDA(cudaStreamSynchronize(st));
     return NK_OK;

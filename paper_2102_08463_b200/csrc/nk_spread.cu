@@ -321,7 +321,8 @@ __global__ void __launch_bounds__(512, 1)
 k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
                const int32_t *__restrict__ sub_stop, const double *__restrict__ pts,
                int64_t pitch, const double2 *__restrict__ cvis, Geom g,
-               double2 *__restrict__ fine, int64_t stage_off, int dbg) {
+               double2 *__restrict__ fine, int64_t stage_off, int dbg,
+               const int32_t *__restrict__ sched) {
     constexpr int WIN = kTileWin, NB = kTileBatch, L = nk_tile_lg(W), TM = (1 << L) - 1;
     constexpr int NWARP = 16;
     static_assert(W + TM <= WIN, "window too small for the tile");
@@ -345,7 +346,7 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
     unsigned char *raw = stg + 2 * SB;
     uint64_t *mbar = reinterpret_cast<uint64_t *>(raw + 3 * RB);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int s = blockIdx.x;
+    const int s = sched ? sched[blockIdx.x] : (int)blockIdx.x;
     cvis += blockIdx.y * pitch;
     fine += blockIdx.y * g.ntot;
     int corner[3];
@@ -753,7 +754,7 @@ int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
             kern<<<dim3((unsigned)p->S, p->ntrans), 512, smem, p->stream>>>(
                 p->d_sub_bin, p->d_sub_start, p->d_sub_stop, (const double *)p->d_pts, p->cap_M,
                 (const double2 *)p->d_cvis, p->geom, (double2 *)fine, stage_off,
-                getenv("NK_DBG") ? atoi(getenv("NK_DBG")) : 0);
+                getenv("NK_DBG") ? atoi(getenv("NK_DBG")) : 0, p->d_sub_sched);
             NK_LAUNCH_CHECK();
             ++*launches;
             return NK_OK;

@@ -64,8 +64,8 @@ typedef struct {
                             gather ("sm", measured faster on B200) */
     int bin_dims[3];     /* 0 = default.  GM-sort plans: the reference's (32,32) /
                             (16,16,2) (binsort.py:34-35).  SM plans: B200-tuned shapes
-                            -- type 1: 2D (16,8), 3D f32 (4,4,4), 3D f64 (16,8,4);
-                            type 2: 2D (32,32), 3D f32 (16,16,4), 3D f64 (7,7,7);
+                            -- type 1: 2D (16,8), 3D f32 (4,4,4), 3D f64 (11,7,7);
+                            type 2: 2D (32,32), 3D f32 (16,16,4), 3D f64 (11,7,7);
                             halved along axes 1/2 while the padded bin exceeds
                             shared memory */
     int max_subproblem;  /* 0 = default.  The reference default is 1024

@@ -267,8 +267,8 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     // (or the 2D one-warp subproblems) resident per SM.  GM / GM-sort and the
     // stage-level bin_sort keep the reference defaults (binsort.py:34-35).
     if (method == NK_SM && !user_bins) {
-        static const int t1_2d[3] = {16, 8, 1}, t1_3s[3] = {4, 4, 4}, t1_3d[3] = {16, 8, 4},
-                         t2_2d[3] = {32, 32, 1}, t2_3s[3] = {16, 16, 4}, t2_3d[3] = {7, 7, 7};
+        static const int t1_2d[3] = {16, 8, 1}, t1_3s[3] = {4, 4, 4}, t1_3d[3] = {11, 7, 7},
+                         t2_2d[3] = {32, 32, 1}, t2_3s[3] = {16, 16, 4}, t2_3d[3] = {11, 7, 7};
         const int *tb = type == 1 ? (dim == 2 ? t1_2d : (precision == NK_SINGLE ? t1_3s : t1_3d))
                                   : (dim == 2 ? t2_2d : (precision == NK_SINGLE ? t2_3s : t2_3d));
         p->nbins = 1;

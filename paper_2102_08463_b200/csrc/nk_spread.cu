@@ -356,7 +356,11 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
     const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
     const int p3 = min(g.m[2], g.n[2] - corner[2]) + 2 * h;
     const int P = p1 * p2 * p3, pstride = p1 * p2;
-    for (int i = threadIdx.x; i < P; i += blockDim.x) buf[i] = make_double2(0.0, 0.0);
+    for (int i = threadIdx.x; i < P && !(dbg & 16); i += blockDim.x) buf[i] = make_double2(0.0, 0.0);
+    // staged rows are read up to 3 points past a segment (operands of the
+    // points beyond it are multiplied by a zeroed c k3): keep them finite
+    for (int i = threadIdx.x; i < 2 * SB / 16; i += blockDim.x)
+        reinterpret_cast<double2 *>(stg)[i] = make_double2(0.0, 0.0);
     const double half = 0.5 * W;
     const int j0 = sub_start[s], j1 = sub_stop[s];
     // stage window rows of points [b, b + nb) into buffer bi: row v = (point
@@ -408,7 +412,7 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
             typedef EsPoly64<W> P;
 #pragma unroll
             for (int r = 0; r < W; ++r) {
-                if (r / PP != part) continue;   // warp-uniform
+                if (r / PP != part || (dbg & 8)) continue;   // warp-uniform
                 double kv;
                 if (r == 0 || r == W - 1) {
                     kv = nk_es(z0 + (2.0 * r / W), g);
@@ -511,30 +515,42 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
             struct Ops {
                 double2 ck;
                 double a0, a8, k2[4];
+                bool act;
             };
+            // lane operand pointers at point q + kp (rows padded to NB + 4
+            // points; advance by 4 points per chunk)
+            const double2 *pck = sck3 + e * NB + q + kp;
+            const double *pa = sk1 + row * KS + q + kp;
+            const double *pb = sk2 + ycol * KS + q + kp;
             auto load = [&](int cq, Ops &o) {
-                const int qp = min(cq + kp, qe - 1);
-                o.ck = sck3[e * NB + qp];
-                if (cq + kp >= qe) o.ck = make_double2(0.0, 0.0);
-                o.a0 = sk1[row * KS + qp];
-                o.a8 = sk1[(8 + row) * KS + qp];
+                const int d = cq - q;
+                o.ck = cq + kp < qe ? pck[d] : make_double2(0.0, 0.0);
+                o.a0 = pa[d];
+                o.a8 = pa[8 * KS + d];
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) o.k2[nt] = sk2[(nt * 4 + ycol) * KS + qp];
+                for (int nt = 0; nt < 4; ++nt) o.k2[nt] = pb[nt * 4 * KS + d];
+            };
+            // B operands k2[y] (c k3[e]) and the plane-activity vote, one
+            // pipeline stage before the DMMAs that consume them
+            auto prep = [&](Ops &o) {
+                // plane e outside every chunk point's footprint: c k3 = 0
+                o.act = !(dbg & 4) && __any_sync(0xffffffffu, o.ck.x != 0.0 || o.ck.y != 0.0);
+                const double ckc = cpart ? o.ck.y : o.ck.x;
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) o.k2[nt] *= ckc;
             };
             auto mma = [&](const Ops &o) {
-                // plane e outside every chunk point's footprint: c k3 = 0
-                if (!(dbg & 4) && __any_sync(0xffffffffu, o.ck.x != 0.0 || o.ck.y != 0.0)) {
-                    const double ckc = cpart ? o.ck.y : o.ck.x;
+                if (o.act) {
 #pragma unroll
                     for (int nt = 0; nt < 4; ++nt) {
-                        const double bv = o.k2[nt] * ckc;
-                        nk_dmma(acc[0][nt][0], acc[0][nt][1], o.a0, bv);
-                        nk_dmma(acc[1][nt][0], acc[1][nt][1], o.a8, bv);
+                        nk_dmma(acc[0][nt][0], acc[0][nt][1], o.a0, o.k2[nt]);
+                        nk_dmma(acc[1][nt][0], acc[1][nt][1], o.a8, o.k2[nt]);
                     }
                 }
             };
             Ops A, B;
             load(q, A);
+            prep(A);
             int cq = q;
             for (;;) {
                 if (cq + 4 >= qe) {
@@ -543,6 +559,7 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
                 }
                 load(cq + 4, B);
                 mma(A);
+                prep(B);
                 cq += 4;
                 if (cq + 4 >= qe) {
                     mma(B);
@@ -550,6 +567,7 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
                 }
                 load(cq + 4, A);
                 mma(B);
+                prep(A);
                 cq += 4;
             }
             q = qe;

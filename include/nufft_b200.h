@@ -80,6 +80,12 @@ typedef struct {
     int n_trans;         /* vectors per execute (cufinufft ntransf); 0 or 1 = one.  The
                             reference has no batching; the paper reuses
                             one setpts across many transforms */
+    int deterministic;   /* nonzero: repeated type-1 executes are bit-identical
+                            (SPEC.md:163).  SM plans merge their padded bins in
+                            colour classes of non-overlapping bins, one launch per
+                            class, so every fine-grid cell is summed in a fixed
+                            order.  Type 2 is always deterministic; GM / GM-sort
+                            type 1 (per-point atomics) is not */
 } nk_opts;
 
 typedef struct {

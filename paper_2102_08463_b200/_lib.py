@@ -28,7 +28,8 @@ class NkOpts(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int), ("bin_dims", ctypes.c_int * 3),
                 ("max_subproblem", ctypes.c_int), ("fine", ctypes.c_int64 * 3),
                 ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
-                ("timing", ctypes.c_int), ("n_trans", ctypes.c_int)]
+                ("timing", ctypes.c_int), ("n_trans", ctypes.c_int),
+                ("deterministic", ctypes.c_int)]
 
 
 class NkPlanInfo(ctypes.Structure):

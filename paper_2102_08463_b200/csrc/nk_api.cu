@@ -69,6 +69,7 @@ void free_plan(nk_plan *p) {
                     p->d_pts_alt, p->d_sort_scr, p->d_work, p->d_cvis, p->d_rec, p->d_sub_sched};
     for (void *b : bufs)
         if (b) cudaFree(b);
+    free(p->h_det_off);
     if (p->fft_ok) cufftDestroy(p->fft);
     if (p->fft_col_ok) cufftDestroy(p->fft_col);
     if (p->d_twiddle) cudaFree(p->d_twiddle);
@@ -171,6 +172,7 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     nk_plan *p = new nk_plan();
     memset((void *)p, 0, sizeof(*p));
     p->ntrans = opts.n_trans > 0 ? opts.n_trans : 1;
+    p->deterministic = opts.deterministic ? 1 : 0;
     p->type = type;
     p->dim = dim;
     p->prec = precision;

@@ -129,6 +129,11 @@ struct nk_plan {
     int32_t *d_sub_bin, *d_sub_start, *d_sub_stop;
     int32_t *d_sub_sched;   // tiled f64 kernels: CTA -> subproblem in Morton order of bins
     int64_t cap_sched;
+    // deterministic type-1 merge: subproblems sorted by (rank in bin, colour
+    // class of non-overlapping bins); launch g covers sched[off[g], off[g+1])
+    int deterministic;
+    int *h_det_off;
+    int n_det;
     int max_sub_smem;       // bytes of dynamic smem for the SM kernels
     int64_t max_pad_cells;  // prod(m_i + 2 halo)
     int64_t start_space;    // footprint-start codes per bin (nk_start_code range)

@@ -9,6 +9,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "nk_device.cuh"
 
@@ -421,6 +422,35 @@ __global__ void k_sched_keys(int S, const int32_t *__restrict__ sub_bin, Geom g,
     const int by = r % g.nb[1], bz = r / g.nb[1];
     keys[s] = (int32_t)(nk_spread_bits3(bx) | (nk_spread_bits3(by) << 1) |
                         (nk_spread_bits3(bz) << 2));
+}
+
+// ---------------------------------------------------------------- K4k
+// Deterministic type-1 merge order: key = rank of the subproblem inside its
+// bin x colours + colour of its bin, colour = per-axis class of bins whose
+// padded extents (m + 2 halo) cannot overlap, periodic seam included
+// (classes b mod c for the first nb - nb mod c bins, one class each for the
+// remainder).  Launched class by class, every fine-grid cell receives at
+// most one merge per launch: the summation order is fixed.
+__global__ void k_det_keys(int S, const int32_t *__restrict__ sub_bin,
+                           const int32_t *__restrict__ nsub_off, Geom g, int3 cc, int3 ncol,
+                           int32_t *__restrict__ keys) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    const int b = sub_bin[s];
+    int c[3] = {b % g.nb[0], 0, 0};
+    const int r = b / g.nb[0];
+    c[1] = g.dim == 3 ? r % g.nb[1] : r;
+    c[2] = g.dim == 3 ? r / g.nb[1] : 0;
+    const int cs[3] = {cc.x, cc.y, cc.z};
+    int col[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const int rem = g.nb[a] % cs[a], reg = g.nb[a] - rem;
+        col[a] = c[a] < reg ? c[a] % cs[a] : cs[a] + (c[a] - reg);
+    }
+    const int color = col[0] + ncol.x * (col[1] + ncol.y * col[2]);
+    const int rank = s - nsub_off[b];
+    keys[s] = rank * (ncol.x * ncol.y * ncol.z) + color;
 }
 
 // ---------------------------------------------------------------- K5
@@ -923,10 +953,57 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
             }
         }
     }
-    // Morton schedule of the subproblems for the tiled f64 kernels (bins
-    // per axis <= 1024; the scratch is free once the visit order is set)
-    if (p->geom.tiled && p->S > 0 && p->dim == 3 && p->nb[0] <= 1024 && p->nb[1] <= 1024 &&
-        p->nb[2] <= 1024 && !getenv("NK_NO_SCHED")) {
+    free(p->h_det_off);
+    p->h_det_off = nullptr;
+    p->n_det = 0;
+    if (p->deterministic && p->type == 1 && p->method == NK_SM && p->S > 0) {
+        // colour classes per axis: ceil((m + 2 halo) / m) residues (+ the
+        // remainder bins), then (rank, colour) keys sorted stably
+        int cs[3] = {1, 1, 1}, nc[3] = {1, 1, 1};
+        for (int a = 0; a < p->dim; ++a) {
+            const int m = p->bin_dims[a];
+            cs[a] = (int)std::min<int64_t>((m + 2 * p->halo + m - 1) / m, p->nb[a]);
+            nc[a] = cs[a] + (int)(p->nb[a] % cs[a]);
+        }
+        if (p->S > p->cap_sched || !p->d_sub_sched) {
+            cudaFree(p->d_sub_sched);
+            p->d_sub_sched = nullptr;
+            NK_CUDA(cudaMalloc((void **)&p->d_sub_sched, 4 * (size_t)p->S));
+            p->cap_sched = p->S;
+        }
+        const int64_t q = p->cap_M;   // (bin, start) scratch, free once the visit order is set
+        int32_t *scr = p->d_sort_scr, *skeys = scr + q;
+        k_det_keys<<<blocks_for(p->S, 256), 256, 0, st>>>((int)p->S, p->d_sub_bin,
+                                                          p->d_nsub_off, p->geom,
+                                                          make_int3(cs[0], cs[1], cs[2]),
+                                                          make_int3(nc[0], nc[1], nc[2]), scr);
+        NK_LAUNCH_CHECK();
+        int maxrank = 1;
+        {
+            std::vector<int32_t> off(nbins + 1);
+            NK_CUDA(cudaMemcpyAsync(off.data(), p->d_nsub_off, 4 * (size_t)(nbins + 1),
+                                    cudaMemcpyDeviceToHost, st));
+            NK_CUDA(cudaStreamSynchronize(st));
+            for (int b = 0; b < nbins; ++b) maxrank = std::max(maxrank, off[b + 1] - off[b]);
+        }
+        const int64_t nkeys = (int64_t)maxrank * nc[0] * nc[1] * nc[2];
+        rc = radix_sort_pairs(p, scr, nullptr, p->S, bits_for(nkeys), skeys, p->d_sub_sched,
+                              scr + 2 * q, scr + 3 * q);
+        if (rc) return rc;
+        std::vector<int32_t> hk((size_t)p->S);
+        NK_CUDA(cudaMemcpyAsync(hk.data(), skeys, 4 * (size_t)p->S, cudaMemcpyDeviceToHost, st));
+        NK_CUDA(cudaStreamSynchronize(st));
+        std::vector<int> offs;
+        for (int64_t i = 0; i < p->S; ++i)
+            if (i == 0 || hk[i] != hk[i - 1]) offs.push_back((int)i);
+        offs.push_back((int)p->S);
+        p->n_det = (int)offs.size() - 1;
+        p->h_det_off = (int *)malloc(sizeof(int) * offs.size());
+        memcpy(p->h_det_off, offs.data(), sizeof(int) * offs.size());
+    } else if (p->geom.tiled && p->S > 0 && p->dim == 3 && p->nb[0] <= 1024 &&
+               p->nb[1] <= 1024 && p->nb[2] <= 1024 && !getenv("NK_NO_SCHED")) {
+        // Morton schedule of the subproblems for the tiled f64 kernels (bins
+        // per axis <= 1024; the scratch is free once the visit order is set)
         if (p->S > p->cap_sched || !p->d_sub_sched) {
             cudaFree(p->d_sub_sched);
             p->d_sub_sched = nullptr;

@@ -7,6 +7,8 @@
 //           padded bin (Eq. (16)) is accumulated in shared memory without
 //           atomics (one warp per subproblem in 2D, plane-owned warps in 3D),
 //           then merged into the grid with periodic wrap (Eq. (17)).
+#include <algorithm>
+
 #include "nk_device.cuh"
 
 namespace {
@@ -88,7 +90,8 @@ __global__ void __launch_bounds__(NW * 32)
 k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
              const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
              const T *__restrict__ pts, int64_t pitch, const typename cplx<T>::t *__restrict__ c,
-             Geom g, typename cplx<T>::t *__restrict__ fine, int64_t stage_off, int nbatch) {
+             Geom g, typename cplx<T>::t *__restrict__ fine, int64_t stage_off, int nbatch,
+             const int32_t *__restrict__ sched, int sched_base) {
     typedef typename cplx<T>::t C;
     constexpr bool XWIN = sizeof(T) == 8 && W <= 16;
     constexpr int XW = 16;                      // x-window width (XWIN)
@@ -104,7 +107,7 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     T *sk2 = sk1 + nbatch * K1P;
     C *sck3 = reinterpret_cast<C *>(sk2 + nbatch * W);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int s = blockIdx.x;
+    const int s = sched ? sched[sched_base + blockIdx.x] : (int)blockIdx.x;
     c += blockIdx.y * g.M;          // batched execute: vector blockIdx.y
     fine += blockIdx.y * g.ntot;
     int corner[3];
@@ -322,7 +325,7 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
                const int32_t *__restrict__ sub_stop, const double *__restrict__ pts,
                int64_t pitch, const double2 *__restrict__ cvis, Geom g,
                double2 *__restrict__ fine, int64_t stage_off, int dbg,
-               const int32_t *__restrict__ sched) {
+               const int32_t *__restrict__ sched, int sched_base) {
     constexpr int WIN = kTileWin, NB = kTileBatch, L = nk_tile_lg(W), TM = (1 << L) - 1;
     constexpr int NWARP = 16;
     static_assert(W + TM <= WIN, "window too small for the tile");
@@ -346,7 +349,7 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
     unsigned char *raw = stg + 2 * SB;
     uint64_t *mbar = reinterpret_cast<uint64_t *>(raw + 3 * RB);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int s = sched ? sched[blockIdx.x] : (int)blockIdx.x;
+    const int s = sched ? sched[sched_base + blockIdx.x] : (int)blockIdx.x;
     cvis += blockIdx.y * pitch;
     fine += blockIdx.y * g.ntot;
     int corner[3];
@@ -639,7 +642,8 @@ __global__ void __launch_bounds__(32)
 k_spread_sm2(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
              const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
              const T *__restrict__ pts, int64_t pitch, const typename cplx<T>::t *__restrict__ c,
-             Geom g, typename cplx<T>::t *__restrict__ fine, int64_t stage_off) {
+             Geom g, typename cplx<T>::t *__restrict__ fine, int64_t stage_off,
+             const int32_t *__restrict__ sched, int sched_base) {
     typedef typename cplx<T>::t C;
     constexpr int NIT = (W * W + 31) / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -648,7 +652,7 @@ k_spread_sm2(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
     T *sk1 = reinterpret_cast<T *>(sbase + 32);
     C *sck2 = reinterpret_cast<C *>(smem_raw + stage_off + 128 + ((32 * W * sizeof(T) + 15) / 16) * 16);
     const int lane = threadIdx.x;
-    const int s = blockIdx.x;
+    const int s = sched ? sched[sched_base + blockIdx.x] : (int)blockIdx.x;
     c += blockIdx.y * g.M;          // batched execute: vector blockIdx.y
     fine += blockIdx.y * g.ntot;
     int corner[3];
@@ -769,12 +773,17 @@ int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
                 M, p->d_vperm, (const double2 *)c, g_M(p), (double2 *)p->d_cvis, p->cap_M);
             NK_LAUNCH_CHECK();
             ++*launches;
-            kern<<<dim3((unsigned)p->S, p->ntrans), 512, smem, p->stream>>>(
-                p->d_sub_bin, p->d_sub_start, p->d_sub_stop, (const double *)p->d_pts, p->cap_M,
-                (const double2 *)p->d_cvis, p->geom, (double2 *)fine, stage_off,
-                getenv("NK_DBG") ? atoi(getenv("NK_DBG")) : 0, p->d_sub_sched);
-            NK_LAUNCH_CHECK();
-            ++*launches;
+            const int dbg = getenv("NK_DBG") ? atoi(getenv("NK_DBG")) : 0;
+            for (int gi = 0; gi < std::max(p->n_det, 1); ++gi) {
+                const int b0 = p->n_det ? p->h_det_off[gi] : 0;
+                const int cnt = p->n_det ? p->h_det_off[gi + 1] - b0 : (int)p->S;
+                kern<<<dim3((unsigned)cnt, p->ntrans), 512, smem, p->stream>>>(
+                    p->d_sub_bin, p->d_sub_start, p->d_sub_stop, (const double *)p->d_pts,
+                    p->cap_M, (const double2 *)p->d_cvis, p->geom, (double2 *)fine, stage_off,
+                    dbg, p->d_sub_sched, b0);
+                NK_LAUNCH_CHECK();
+                ++*launches;
+            }
             return NK_OK;
         }
     }
@@ -786,9 +795,15 @@ int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
         NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         int64_t stage_off = (p->max_pad_cells * (int64_t)sizeof(C) + 15) / 16 * 16;
-        kern<<<dim3((unsigned)p->S, p->ntrans), NW * 32, smem, p->stream>>>(
-            p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm, (const T *)p->d_pts,
-            p->cap_M, (const C *)c, p->geom, (C *)fine, stage_off, nk_sm3_batch(p->prec));
+        for (int gi = 0; gi < std::max(p->n_det, 1); ++gi) {
+            const int b0 = p->n_det ? p->h_det_off[gi] : 0;
+            const int cnt = p->n_det ? p->h_det_off[gi + 1] - b0 : (int)p->S;
+            kern<<<dim3((unsigned)cnt, p->ntrans), NW * 32, smem, p->stream>>>(
+                p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm, (const T *)p->d_pts,
+                p->cap_M, (const C *)c, p->geom, (C *)fine, stage_off, nk_sm3_batch(p->prec),
+                p->n_det ? p->d_sub_sched : nullptr, b0);
+            if (gi + 1 < p->n_det) ++*launches;
+        }
     } else if (p->method == NK_SM && D == 2) {
         if (p->S == 0) return NK_OK;
         size_t smem = (size_t)p->max_sub_smem;
@@ -796,9 +811,15 @@ int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
         NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         int64_t stage_off = (p->max_pad_cells * (int64_t)sizeof(C) + 15) / 16 * 16;
-        kern<<<dim3((unsigned)p->S, p->ntrans), 32, smem, p->stream>>>(
-            p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm, (const T *)p->d_pts,
-            p->cap_M, (const C *)c, p->geom, (C *)fine, stage_off);
+        for (int gi = 0; gi < std::max(p->n_det, 1); ++gi) {
+            const int b0 = p->n_det ? p->h_det_off[gi] : 0;
+            const int cnt = p->n_det ? p->h_det_off[gi + 1] - b0 : (int)p->S;
+            kern<<<dim3((unsigned)cnt, p->ntrans), 32, smem, p->stream>>>(
+                p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm, (const T *)p->d_pts,
+                p->cap_M, (const C *)c, p->geom, (C *)fine, stage_off,
+                p->n_det ? p->d_sub_sched : nullptr, b0);
+            if (gi + 1 < p->n_det) ++*launches;
+        }
     } else {
         const int32_t *perm = p->method == NK_GM ? nullptr : p->d_vperm;
         k_spread_gm<T, D, W><<<dim3((M + 255) / 256, p->ntrans), 256, 0, p->stream>>>(

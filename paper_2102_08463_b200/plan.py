@@ -104,11 +104,15 @@ class TransformPlan:
             the reference has no batching).  Inputs and
             outputs then carry a leading axis of length n_trans; the sort and
             subproblems of one set_points serve every vector.
+        deterministic: type-1 SM plans merge their subproblems in colour
+            classes of non-overlapping bins (one launch each), so repeated
+            executes are bit-identical.  Type 2 is always
+            deterministic; GM / GM-sort type 1 is not.
     """
 
     def __init__(self, nufft_type, modes, epsilon, method="default", precision="double",
                  workers=0, *, bin_dims=None, max_subproblem=None, fine=None, device=None,
-                 timing=False, n_trans=1):
+                 timing=False, n_trans=1, deterministic=False):
         if int(workers) < 0:
             raise ValueError(f"worker count must be >= 0, got {workers}")
         if precision not in _COMPLEX:
@@ -131,6 +135,7 @@ class TransformPlan:
         if int(n_trans) < 1:
             raise ValueError(f"n_trans must be >= 1, got {n_trans}")
         opts.n_trans = int(n_trans)
+        opts.deterministic = 1 if deterministic else 0
         if bin_dims is not None:
             bin_dims = tuple(int(m) for m in bin_dims)
             if len(bin_dims) != d or any(m < 1 for m in bin_dims):

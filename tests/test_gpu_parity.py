@@ -641,3 +641,33 @@ def test_fft_deconvolve_stage_matches_execute(nk, orc, modes, prec):
     tol = 2e-6 if prec == "single" else 1e-13
     assert orc.rel_l2_error(out.cpu().numpy(), ref.cpu().numpy()) < tol
     assert orc.rel_l2_error(out2.cpu().numpy(), ref.cpu().numpy()) < tol
+
+
+@pytest.mark.parametrize("modes,prec,eps,dist", [((24, 20, 16), "double", 1e-12, "rand"),
+                                                 ((24, 20, 16), "double", 1e-12, "cluster"),
+                                                 ((20, 20, 20), "single", 1e-6, "rand"),
+                                                 ((64, 48), "single", 1e-5, "cluster"),
+                                                 ((64, 48), "double", 1e-9, "rand")])
+def test_deterministic_type1_bit_identical(nk, orc, modes, prec, eps, dist):
+    """deterministic=True: SM type-1 plans merge their padded
+    bins one colour class of non-overlapping bins per launch, so repeated
+    executes -- and a second plan on the same points -- are bit-identical,
+    and equal the default plan to rounding."""
+    grid = orc.make_grid(modes, eps, prec)
+    rdt = np.float32 if prec == "single" else np.float64
+    cdt = np.complex64 if prec == "single" else np.complex128
+    M = 40000
+    pts = orc.gen_points(dist, M, grid, 61, rdt)
+    c = orc.gen_strengths(M, 62, cdt)
+    p = nk.make_plan(1, modes, eps, "sm", prec, deterministic=True)
+    p.set_points(pts)
+    outs = [np.asarray(p.execute(c)).copy() for _ in range(3)]
+    q = nk.make_plan(1, modes, eps, "sm", prec, deterministic=True)
+    q.set_points(pts)
+    outs.append(np.asarray(q.execute(c)))
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.uint8), outs[0].view(np.uint8))
+    r = nk.make_plan(1, modes, eps, "sm", prec)
+    r.set_points(pts)
+    tol = 1e-6 if prec == "single" else 1e-13
+    assert orc.rel_l2_error(outs[0], r.execute(c)) < tol

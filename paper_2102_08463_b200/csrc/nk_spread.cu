@@ -319,15 +319,19 @@ inline int64_t g_M(const nk_plan *p) { return p->M; }
 // double-buffered: batch b + 1 is staged between the barrier that retires
 // batch b - 1 and the DMMAs of batch b.  Flush = native f64 reductions, one
 // padded-bin row per warp pass (Eq. 17).
-template <int W>
-__global__ void __launch_bounds__(512, 1)
+template <int W, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
 k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
                const int32_t *__restrict__ sub_stop, const double *__restrict__ pts,
                int64_t pitch, const double2 *__restrict__ cvis, Geom g,
                double2 *__restrict__ fine, int64_t stage_off, int dbg,
                const int32_t *__restrict__ sched, int sched_base) {
     constexpr int WIN = kTileWin, NB = kTileBatch, L = nk_tile_lg(W), TM = (1 << L) - 1;
-    constexpr int NWARP = 16;
+    // NW warps; warp w owns the window planes z == w (mod NW): PL planes per
+    // warp and group (16 warps x 1 plane, or 8 warps x 2 planes sharing the
+    // A / k2 operand loads)
+    constexpr int NWARP = NW, PL = WIN / NW;
+    static_assert(WIN % NW == 0, "planes per warp");
     static_assert(W + TM <= WIN, "window too small for the tile");
     static_assert(NB <= 32, "one boundary mask word per batch");
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -396,10 +400,10 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
         // a row's W values are split over 4 warps (pieces [part PP, part PP +
         // PP)), each warp covering 32 rows, so the staging lag of a warp is a
         // quarter of a row
-        constexpr int NPART = 4, PP = (W + NPART - 1) / NPART;
+        constexpr int NPART = NW == 16 ? 4 : 2, PP = (W + NPART - 1) / NPART;
         const int v = (int)threadIdx.x;
         const int part = (v >> 5) & (NPART - 1);
-        const int rowi = ((v >> 7) << 5) | (v & 31);
+        const int rowi = (((v >> 5) / NPART) << 5) | (v & 31);
         if (rowi < nb * 3) {
             const int q = rowi / 3, ax = rowi - 3 * q;
             const double u = ru[ax * RU + q];
@@ -502,13 +506,15 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
         const int4 g0 = sinfo[q];
         const int grp = g0.x;
         const int a1 = g0.y & 0xff, a2 = (g0.y >> 8) & 0xff, a3 = g0.y >> 16;
-        const int e = (warp - a3) & (WIN - 1);   // the warp's window plane
+        const int e = (warp - a3) & (NW - 1);    // the warp's first window plane
         // lane (row lane / 4, column pair lane % 4) holds cell (x, y) as (re, im)
-        double acc[2][4][2];
+        double acc[PL][2][4][2];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int pl = 0; pl < PL; ++pl)
 #pragma unroll
-            for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) acc[pl][mt][nt][0] = acc[pl][mt][nt][1] = 0.0;
         for (;;) {
             // the group's segment of this batch: [q, qe)
             const unsigned rest = q + 1 < 32 ? bnd >> (q + 1) : 0u;
@@ -516,9 +522,9 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
             // chunks of 4 points (lane k-index = point cq + kp); the next
             // chunk's operands load while the current chunk's DMMAs issue
             struct Ops {
-                double2 ck;
-                double a0, a8, k2[4];
-                bool act;
+                double2 ck[PL];
+                double a0, a8, k2[4], bv[PL][4];
+                bool act[PL];
             };
             // lane operand pointers at point q + kp (rows padded to NB + 4
             // points; advance by 4 points per chunk)
@@ -527,27 +533,36 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
             const double *pb = sk2 + ycol * KS + q + kp;
             auto load = [&](int cq, Ops &o) {
                 const int d = cq - q;
-                o.ck = cq + kp < qe ? pck[d] : make_double2(0.0, 0.0);
+#pragma unroll
+                for (int pl = 0; pl < PL; ++pl)
+                    o.ck[pl] = cq + kp < qe ? pck[pl * NW * NB + d] : make_double2(0.0, 0.0);
                 o.a0 = pa[d];
                 o.a8 = pa[8 * KS + d];
 #pragma unroll
                 for (int nt = 0; nt < 4; ++nt) o.k2[nt] = pb[nt * 4 * KS + d];
             };
-            // B operands k2[y] (c k3[e]) and the plane-activity vote, one
+            // B operands k2[y] (c k3[e]) and the plane-activity votes, one
             // pipeline stage before the DMMAs that consume them
             auto prep = [&](Ops &o) {
-                // plane e outside every chunk point's footprint: c k3 = 0
-                o.act = !(dbg & 4) && __any_sync(0xffffffffu, o.ck.x != 0.0 || o.ck.y != 0.0);
-                const double ckc = cpart ? o.ck.y : o.ck.x;
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) o.k2[nt] *= ckc;
+                for (int pl = 0; pl < PL; ++pl) {
+                    // plane outside every chunk point's footprint: c k3 = 0
+                    o.act[pl] = !(dbg & 4) && __any_sync(0xffffffffu, o.ck[pl].x != 0.0 ||
+                                                                         o.ck[pl].y != 0.0);
+                    const double ckc = cpart ? o.ck[pl].y : o.ck[pl].x;
+#pragma unroll
+                    for (int nt = 0; nt < 4; ++nt) o.bv[pl][nt] = o.k2[nt] * ckc;
+                }
             };
             auto mma = [&](const Ops &o) {
-                if (o.act) {
 #pragma unroll
-                    for (int nt = 0; nt < 4; ++nt) {
-                        nk_dmma(acc[0][nt][0], acc[0][nt][1], o.a0, o.k2[nt]);
-                        nk_dmma(acc[1][nt][0], acc[1][nt][1], o.a8, o.k2[nt]);
+                for (int pl = 0; pl < PL; ++pl) {
+                    if (o.act[pl]) {
+#pragma unroll
+                        for (int nt = 0; nt < 4; ++nt) {
+                            nk_dmma(acc[pl][0][nt][0], acc[pl][0][nt][1], o.a0, o.bv[pl][nt]);
+                            nk_dmma(acc[pl][1][nt][0], acc[pl][1][nt][1], o.a8, o.bv[pl][nt]);
+                        }
                     }
                 }
             };
@@ -586,25 +601,29 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
         // (the window moved since the warp's last flush: a cell another lane
         // wrote then may be this lane's now -- order the warp's accesses)
         __syncwarp();
-        const int zpl = a3 + e;
-        if (zpl < p3 && !(dbg & 2)) {
-            double2 *pl = buf + zpl * pstride + (a2 + kp) * p1 + a1 + row;
-            bool ok[2][4];
-            double2 v[2][4];
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
+        for (int pl = 0; pl < PL; ++pl) {
+            const int zpl = a3 + e + pl * NW;
+            if (zpl < p3 && !(dbg & 2)) {
+                double2 *pp = buf + zpl * pstride + (a2 + kp) * p1 + a1 + row;
+                bool ok[2][4];
+                double2 v[2][4];
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) {
-                    ok[mt][nt] = a1 + mt * 8 + row < p1 && a2 + nt * 4 + kp < p2;
-                    v[mt][nt] = ok[mt][nt] ? pl[nt * 4 * p1 + mt * 8] : make_double2(0.0, 0.0);
-                }
+                for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
+                    for (int nt = 0; nt < 4; ++nt) {
+                        ok[mt][nt] = a1 + mt * 8 + row < p1 && a2 + nt * 4 + kp < p2;
+                        v[mt][nt] = ok[mt][nt] ? pp[nt * 4 * p1 + mt * 8] : make_double2(0.0, 0.0);
+                    }
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt)
-                    if (ok[mt][nt])
-                        pl[nt * 4 * p1 + mt * 8] = make_double2(v[mt][nt].x + acc[mt][nt][0],
-                                                                v[mt][nt].y + acc[mt][nt][1]);
+                for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 4; ++nt)
+                        if (ok[mt][nt])
+                            pp[nt * 4 * p1 + mt * 8] =
+                                make_double2(v[mt][nt].x + acc[pl][mt][nt][0],
+                                             v[mt][nt].y + acc[pl][mt][nt][1]);
+            }
         }
     }
     // merge with periodic wrap (Eq. 17): one padded-bin row per thread as
@@ -757,7 +776,11 @@ int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
         if (p->method == NK_SM && p->geom.tiled) {
             if (p->S == 0) return NK_OK;
             size_t smem = (size_t)p->max_sub_smem;
-            auto kern = k_spread_tiled<W>;
+            // 16 warps x one window plane (default; NK_SPREAD_WARPS=8: 8 warps
+            // x 2 planes sharing the A / k2 loads, measured 3 % slower)
+            const char *ew = getenv("NK_SPREAD_WARPS");
+            const int nw = (ew && atoi(ew) == 8) ? 8 : 16;
+            auto kern = nw == 16 ? k_spread_tiled<W, 16> : k_spread_tiled<W, 8>;
             NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
             int64_t stage_off = (p->max_pad_cells * (int64_t)sizeof(C) + 15) / 16 * 16;
@@ -777,7 +800,7 @@ int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
             for (int gi = 0; gi < std::max(p->n_det, 1); ++gi) {
                 const int b0 = p->n_det ? p->h_det_off[gi] : 0;
                 const int cnt = p->n_det ? p->h_det_off[gi + 1] - b0 : (int)p->S;
-                kern<<<dim3((unsigned)cnt, p->ntrans), 512, smem, p->stream>>>(
+                kern<<<dim3((unsigned)cnt, p->ntrans), nw * 32, smem, p->stream>>>(
                     p->d_sub_bin, p->d_sub_start, p->d_sub_stop, (const double *)p->d_pts,
                     p->cap_M, (const double2 *)p->d_cvis, p->geom, (double2 *)fine, stage_off,
                     dbg, p->d_sub_sched, b0);

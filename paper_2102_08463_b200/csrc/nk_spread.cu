@@ -363,11 +363,6 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
     const int p2 = min(g.m[1], g.n[1] - corner[1]) + 2 * h;
     const int p3 = min(g.m[2], g.n[2] - corner[2]) + 2 * h;
     const int P = p1 * p2 * p3, pstride = p1 * p2;
-    for (int i = threadIdx.x; i < P && !(dbg & 16); i += blockDim.x) buf[i] = make_double2(0.0, 0.0);
-    // staged rows are read up to 3 points past a segment (operands of the
-    // points beyond it are multiplied by a zeroed c k3): keep them finite
-    for (int i = threadIdx.x; i < 2 * SB / 16; i += blockDim.x)
-        reinterpret_cast<double2 *>(stg)[i] = make_double2(0.0, 0.0);
     const double half = 0.5 * W;
     const int j0 = sub_start[s], j1 = sub_stop[s];
     // stage window rows of points [b, b + nb) into buffer bi: row v = (point
@@ -452,18 +447,22 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
         }
     };
     // batch state: batch kb = [j0 + kb NB, +nb) in staging buffer kb & 1;
-    // batch kb + 1 is staged, batch kb + 2's raw inputs are in flight
+    // batch kb + 1 is staged, batch kb + 2's raw inputs are in flight.  The
+    // first three batches' copies start before the bin is zeroed
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int i = 0; i < 3; ++i) nk_mbar_init(mbar + i, 1);
         nk_fence_mbar_init();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
         issue(0);
         issue(1);
         issue(2);
     }
+    for (int i = threadIdx.x; i < P && !(dbg & 16); i += blockDim.x) buf[i] = make_double2(0.0, 0.0);
+    // staged rows are read up to 3 points past a segment (operands of the
+    // points beyond it are multiplied by a zeroed c k3): keep them finite
+    for (int i = threadIdx.x; i < 2 * SB / 16; i += blockDim.x)
+        reinterpret_cast<double2 *>(stg)[i] = make_double2(0.0, 0.0);
+    __syncthreads();   // barriers initialised (and the bin zeroed)
     int kb = 0;
     int nb = min(NB, j1 - j0);
     if (nb > 0) stage(0, 0);

@@ -381,7 +381,7 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     NK_ALLOC(p->d_fine, p->n_tot * p->csize * p->ntrans);
     // TMA tensor map of the fine grid for the tiled interpolation: one
     // cp.async.bulk.tensor box per (non-wrapping) padded bin
-    if (p->geom.tiled && type == 2) {
+    if (type == 2 && method == NK_SM) {
         static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
         if (!encode) {
             cudaDriverEntryPointQueryResult q;
@@ -392,20 +392,24 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
                 encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
             cudaGetLastError();
         }
+        // the grid as reals (2 n1, n2, n3, n_trans); 2D grids have n3 = 1
         const int h2 = 2 * p->halo;
+        const cuuint64_t rs = precision == NK_DOUBLE ? 8 : 4;
         const cuuint64_t dims[4] = {(cuuint64_t)(2 * p->n[0]), (cuuint64_t)p->n[1],
                                     (cuuint64_t)p->n[2], (cuuint64_t)p->ntrans};
-        const cuuint64_t strides[3] = {(cuuint64_t)(16 * p->n[0]),
-                                       (cuuint64_t)(16 * p->n[0] * p->n[1]),
-                                       (cuuint64_t)(16 * p->n_tot)};
+        const cuuint64_t strides[3] = {(cuuint64_t)(2 * rs * p->n[0]),
+                                       (cuuint64_t)(2 * rs * p->n[0] * p->n[1]),
+                                       (cuuint64_t)(2 * rs * p->n_tot)};
         const cuuint32_t box[4] = {(cuuint32_t)(2 * (p->bin_dims[0] + h2)),
                                    (cuuint32_t)(p->bin_dims[1] + h2),
-                                   (cuuint32_t)(p->bin_dims[2] + h2), 1};
+                                   (cuuint32_t)(dim == 3 ? p->bin_dims[2] + h2 : 1), 1};
         const cuuint32_t estr[4] = {1, 1, 1, 1};
         p->tmap_ok = encode && box[0] <= 256 && box[1] <= 256 && box[2] <= 256 &&
-                     (box[0] * 8) % 16 == 0 &&
-                     encode(&p->tmap_fine, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, p->d_fine, dims,
-                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     (box[0] * rs) % 16 == 0 && strides[0] % 16 == 0 &&
+                     encode(&p->tmap_fine,
+                            precision == NK_DOUBLE ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                                   : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                            4, p->d_fine, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }

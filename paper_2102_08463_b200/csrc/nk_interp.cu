@@ -127,11 +127,16 @@ k_interp_staged(int S, const int32_t *__restrict__ sub_bin, const int32_t *__res
                 const int32_t *__restrict__ sub_stop, const int32_t *__restrict__ perm,
                 const T *__restrict__ pts, int64_t pitch,
                 const typename cplx<T>::t *__restrict__ fine, Geom g,
-                typename cplx<T>::t *__restrict__ out, int buf_cells, int *__restrict__ work) {
+                typename cplx<T>::t *__restrict__ out, int buf_cells, int *__restrict__ work,
+                const __grid_constant__ CUtensorMap tmap, int use_tma) {
     typedef typename cplx<T>::t C;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int sh_next;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    // buffers at 128-byte aligned strides (TMA destinations), then the two
+    // buffers' mbarriers and the work-counter slot
+    const int bstride = (buf_cells * (int)sizeof(C) + 127) / 128 * 128 / (int)sizeof(C);
     C *bufs = reinterpret_cast<C *>(smem_raw);
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(bufs + NBUF * bstride);
+    int &sh_next = *reinterpret_cast<int *>(mbar + 2);
     const int h = g.halo;
     const uint64_t keep = nk_policy_evict_last();
     fine += blockIdx.y * g.ntot;   // batched execute: vector blockIdx.y
@@ -141,21 +146,64 @@ k_interp_staged(int S, const int32_t *__restrict__ sub_bin, const int32_t *__res
     // unclaimed one from a counter (balanced tails for uneven subproblems)
     int s = blockIdx.x;
     int cur = 0;
-    if (threadIdx.x == 0) sh_next = atomicAdd(work, 1) + gridDim.x;
-    if (s < S) stage_padded_bin<T, D>(bufs, fine, g, sub_bin[s]);
+    // a full, non-wrapping padded bin arrives as one TMA box (mbarrier of its
+    // buffer, phase bit per buffer); other bins by cp.async per cell
+    unsigned tma_used = 0, phase = 0;   // bit b: buffer b's pending load is TMA / its parity
+    // the descriptor's address in parameter space, taken outside the lambda
+    // (a by-reference capture would copy the parameter to local memory,
+    // which TMA cannot read)
+    const CUtensorMap *tm = &tmap;
+    auto load = [&, tm](int b, int ss) {
+        int corner[3];
+        nk_bin_corner(sub_bin[ss], g, corner);
+        const int o1 = corner[0] - h, o2 = corner[1] - h, o3 = D == 3 ? corner[2] - h : 0;
+        const bool full = corner[0] + g.m[0] <= g.n[0] && corner[1] + g.m[1] <= g.n[1] &&
+                          (D == 2 || corner[2] + g.m[2] <= g.n[2]);
+        // (single-buffered instantiations only: the double-buffered ones
+        // raised illegal-instruction faults at the TMA issue on B200)
+        const bool tma = NBUF == 1 && use_tma && full && o1 >= 0 && o2 >= 0 && o3 >= 0 &&
+                         o1 + g.m[0] + 2 * h <= g.n[0] && o2 + g.m[1] + 2 * h <= g.n[1] &&
+                         (D == 2 || o3 + g.m[2] + 2 * h <= g.n[2]);
+        if (tma) {
+            tma_used |= 1u << b;
+            if (threadIdx.x == 0) {
+                const int cells = (g.m[0] + 2 * h) * (g.m[1] + 2 * h) * (D == 3 ? g.m[2] + 2 * h : 1);
+                nk_fence_proxy_async();
+                nk_mbar_expect_tx(mbar + b, (unsigned)(cells * (int)sizeof(C)));
+                nk_tma_load_4d(bufs + b * bstride, tm, 2 * o1, o2, o3, blockIdx.y, mbar + b);
+            }
+        } else {
+            tma_used &= ~(1u << b);
+            stage_padded_bin<T, D>(bufs + b * bstride, fine, g, sub_bin[ss]);
+        }
+    };
+    auto wait_tma = [&](int b) {
+        if (tma_used >> b & 1u) {
+            nk_mbar_wait(mbar + b, (phase >> b) & 1u);
+            phase ^= 1u << b;
+        }
+    };
+    if (threadIdx.x == 0) {
+        nk_mbar_init(mbar, 1);
+        nk_mbar_init(mbar + 1, 1);
+        nk_fence_mbar_init();
+        sh_next = atomicAdd(work, 1) + gridDim.x;
+    }
+    if (s < S) load(0, s);
     nk_cp_async_commit();
     __syncthreads();
     int sn = sh_next;
     while (s < S) {
         if (NBUF == 2) {
-            if (sn < S) stage_padded_bin<T, D>(bufs + (cur ^ 1) * buf_cells, fine, g, sub_bin[sn]);
+            if (sn < S) load(cur ^ 1, sn);
             nk_cp_async_commit();
             nk_cp_async_wait<1>();
         } else {
             nk_cp_async_wait<0>();
         }
+        wait_tma(cur);
         __syncthreads();
-        const C *buf = bufs + cur * buf_cells;
+        const C *buf = bufs + cur * bstride;
         int corner[3];
         nk_bin_corner(sub_bin[s], g, corner);
         const int p1 = min(g.m[0], g.n[0] - corner[0]) + 2 * h;
@@ -221,7 +269,7 @@ k_interp_staged(int S, const int32_t *__restrict__ sub_bin, const int32_t *__res
         if (NBUF == 2) {
             cur ^= 1;
         } else if (sn < S) {
-            stage_padded_bin<T, D>(bufs, fine, g, sub_bin[sn]);
+            load(0, sn);
             nk_cp_async_commit();
         }
         s = sn;
@@ -640,7 +688,7 @@ int launch_w(nk_plan *p, const void *fine, void *out, int *launches) {
         }
         // double-buffer when two padded bins leave room for a useful occupancy
         const bool two = 2 * one <= 100 * 1024;
-        const size_t smem = two ? 2 * one : one;
+        const size_t smem = (two ? 2 * (one + 128) : one + 128) + 64;   // + alignment, mbarriers
         auto kern = two ? k_interp_staged<T, D, W, 2> : k_interp_staged<T, D, W, 1>;
         NK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
@@ -651,10 +699,11 @@ int launch_w(nk_plan *p, const void *fine, void *out, int *launches) {
         NK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
         const int64_t grid = std::min<int64_t>(p->S, (int64_t)std::max(per_sm, 1) * nsm);
         NK_CUDA(cudaMemsetAsync(p->d_work, 0, sizeof(int) * p->ntrans, p->stream));
+        const int use_tma = p->tmap_ok && fine == p->d_fine && !getenv("NK_NO_TMA");
         kern<<<dim3((unsigned)grid, p->ntrans), threads, smem, p->stream>>>(
             (int)p->S, p->d_sub_bin, p->d_sub_start, p->d_sub_stop, p->d_vperm,
             (const T *)p->d_pts, p->cap_M, (const C *)fine, p->geom, (C *)out,
-            (int)(one / sizeof(C)), p->d_work);
+            (int)(one / sizeof(C)), p->d_work, p->tmap_fine, use_tma);
     } else {
         const int32_t *perm = p->method == NK_GM ? nullptr : p->d_vperm;
         k_interp_gm<T, D, W><<<dim3((M + 255) / 256, p->ntrans), 256, 0, p->stream>>>(

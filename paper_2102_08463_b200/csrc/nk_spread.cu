@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
 k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ sub_start,
                const int32_t *__restrict__ sub_stop, const double *__restrict__ pts,
                int64_t pitch, const double2 *__restrict__ cvis, Geom g,
-               double2 *__restrict__ fine, int64_t stage_off, int dbg,
+               double2 *__restrict__ fine, int64_t stage_off,
                const int32_t *__restrict__ sched, int sched_base) {
     constexpr int WIN = kTileWin, NB = kTileBatch, L = nk_tile_lg(W), TM = (1 << L) - 1;
     // NW warps; warp w owns the window planes z == w (mod NW): PL planes per
@@ -414,7 +414,7 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
             typedef EsPoly64<W> P;
 #pragma unroll
             for (int r = 0; r < W; ++r) {
-                if (r / PP != part || (dbg & 8)) continue;   // warp-uniform
+                if (r / PP != part) continue;   // warp-uniform
                 double kv;
                 if (r == 0 || r == W - 1) {
                     kv = nk_es(z0 + (2.0 * r / W), g);
@@ -457,7 +457,7 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
         issue(1);
         issue(2);
     }
-    for (int i = threadIdx.x; i < P && !(dbg & 16); i += blockDim.x) buf[i] = make_double2(0.0, 0.0);
+    for (int i = threadIdx.x; i < P; i += blockDim.x) buf[i] = make_double2(0.0, 0.0);
     // staged rows are read up to 3 points past a segment (operands of the
     // points beyond it are multiplied by a zeroed c k3): keep them finite
     for (int i = threadIdx.x; i < 2 * SB / 16; i += blockDim.x)
@@ -546,7 +546,7 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
 #pragma unroll
                 for (int pl = 0; pl < PL; ++pl) {
                     // plane outside every chunk point's footprint: c k3 = 0
-                    o.act[pl] = !(dbg & 4) && __any_sync(0xffffffffu, o.ck[pl].x != 0.0 ||
+                    o.act[pl] = __any_sync(0xffffffffu, o.ck[pl].x != 0.0 ||
                                                                          o.ck[pl].y != 0.0);
                     const double ckc = cpart ? o.ck[pl].y : o.ck[pl].x;
 #pragma unroll
@@ -603,7 +603,7 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
 #pragma unroll
         for (int pl = 0; pl < PL; ++pl) {
             const int zpl = a3 + e + pl * NW;
-            if (zpl < p3 && !(dbg & 2)) {
+            if (zpl < p3) {
                 double2 *pp = buf + zpl * pstride + (a2 + kp) * p1 + a1 + row;
                 bool ok[2][4];
                 double2 v[2][4];
@@ -631,7 +631,7 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
     __syncthreads();
     const int o1 = corner[0] - h, o2 = corner[1] - h, o3 = corner[2] - h;
     bool issued = false;
-    for (int r = threadIdx.x; r < p2 * p3 && !(dbg & 1); r += blockDim.x) {
+    for (int r = threadIdx.x; r < p2 * p3; r += blockDim.x) {
         const int zz = r / p2, yy = r - zz * p2;
         double2 *rowp = fine + ((int64_t)nk_wrap(o3 + zz, g.n[2]) * g.n[1] +
                                 nk_wrap(o2 + yy, g.n[1])) * (int64_t)g.n[0];
@@ -795,14 +795,13 @@ int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
                 M, p->d_vperm, (const double2 *)c, g_M(p), (double2 *)p->d_cvis, p->cap_M);
             NK_LAUNCH_CHECK();
             ++*launches;
-            const int dbg = getenv("NK_DBG") ? atoi(getenv("NK_DBG")) : 0;
             for (int gi = 0; gi < std::max(p->n_det, 1); ++gi) {
                 const int b0 = p->n_det ? p->h_det_off[gi] : 0;
                 const int cnt = p->n_det ? p->h_det_off[gi + 1] - b0 : (int)p->S;
                 kern<<<dim3((unsigned)cnt, p->ntrans), nw * 32, smem, p->stream>>>(
                     p->d_sub_bin, p->d_sub_start, p->d_sub_stop, (const double *)p->d_pts,
                     p->cap_M, (const double2 *)p->d_cvis, p->geom, (double2 *)fine, stage_off,
-                    dbg, p->d_sub_sched, b0);
+                    p->d_sub_sched, b0);
                 NK_LAUNCH_CHECK();
                 ++*launches;
             }

@@ -379,7 +379,7 @@ k_interp_xwin(int S, const int32_t *__restrict__ sub_bin, const int32_t *__restr
               typename cplx<T>::t *__restrict__ out, int buf_cells, int *__restrict__ work) {
     typedef typename cplx<T>::t C;
     constexpr int XW = 16, NB = NK_XWIN_NB, XG = NK_XWIN_G, NWARP = NK_XWIN_WARPS;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ int sh_next;
     C *buf = reinterpret_cast<C *>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -477,7 +477,7 @@ k_interp_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
     constexpr int CS = 8;
     auto pos = [](int c, int q) { return c * CS + (q ^ (((c >> 1) & 1) << 2)); };
     static_assert(W + TM <= WIN, "window too small for the tile");
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     double2 *buf = reinterpret_cast<double2 *>(smem_raw);
     // per warp: k1 / k2 / k3 rows [3][16 cells][CS]; chunk starts
     double *wst = reinterpret_cast<double *>(smem_raw + stage_off) +

@@ -170,7 +170,7 @@ constexpr int nk_sm3_warps(int w) { return w <= 8 ? 2 : w; }
 // 2^L the largest power of two such that w + 2^L - 1 <= 16.
 constexpr int kTileWin = 16;
 #ifndef NK_TILE_NB
-#define NK_TILE_NB 40
+#define NK_TILE_NB 32
 #endif
 constexpr int kTileBatch = NK_TILE_NB;   // points per staged batch (two buffers)
 constexpr int kTileMsub = 1024;          // max subproblem of the tiled interp (chunk table)

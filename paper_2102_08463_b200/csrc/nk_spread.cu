@@ -333,7 +333,7 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
     constexpr int NWARP = NW, PL = WIN / NW;
     static_assert(WIN % NW == 0, "planes per warp");
     static_assert(W + TM <= WIN, "window too small for the tile");
-    static_assert(NB <= 64, "one 64-bit boundary mask per batch");
+    static_assert(NB <= 32, "one boundary mask word per batch");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2 *buf = reinterpret_cast<double2 *>(smem_raw);
     // two staging buffers: info [NB], k1 rows [NB][16], k2 rows [NB][16],
@@ -473,17 +473,11 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
     const double2 *sck3 = sck3_of(0);
     // group boundaries of the current batch as a bit mask (bit q: point q
     // starts a new group), so the chunk loop knows its segment [q, qe)
-    unsigned long long bnd = 0;
+    unsigned bnd = 0;
     auto boundaries = [&]() {
         const int ga = lane < nb ? sinfo[lane].x : -1;
-        const int gb = lane + 32 < nb ? sinfo[lane + 32].x : -1;
         const int pa = __shfl_up_sync(0xffffffffu, ga, 1);
-        const int pb = __shfl_up_sync(0xffffffffu, gb, 1);
-        const int la = __shfl_sync(0xffffffffu, ga, 31);
-        const bool fa = lane < nb && (lane == 0 || ga != pa);
-        const bool fb = lane + 32 < nb && gb != (lane == 0 ? la : pb);
-        bnd = (unsigned long long)__ballot_sync(0xffffffffu, fa) |
-              ((unsigned long long)__ballot_sync(0xffffffffu, fb) << 32);
+        bnd = __ballot_sync(0xffffffffu, lane < nb && (lane == 0 || ga != pa));
     };
     // retire the current batch, switch to the staged one, stage the next
     auto advance = [&]() {
@@ -522,8 +516,8 @@ k_spread_tiled(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ 
                 for (int nt = 0; nt < 4; ++nt) acc[pl][mt][nt][0] = acc[pl][mt][nt][1] = 0.0;
         for (;;) {
             // the group's segment of this batch: [q, qe)
-            const unsigned long long rest = q + 1 < 64 ? bnd >> (q + 1) : 0ull;
-            const int qe = rest ? min(nb, q + __ffsll((long long)rest)) : nb;
+            const unsigned rest = q + 1 < 32 ? bnd >> (q + 1) : 0u;
+            const int qe = rest ? min(nb, q + __ffs(rest)) : nb;
             // chunks of 4 points (lane k-index = point cq + kp); the next
             // chunk's operands load while the current chunk's DMMAs issue
             struct Ops {

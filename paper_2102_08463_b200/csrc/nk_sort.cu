@@ -32,70 +32,88 @@ constexpr int SCAN_CHUNK = SCAN_BLOCK * SCAN_ITEMS;
 // unsorted (GM) plans count here (warp-aggregated atomics); sorted plans
 // derive counts/starts from the sorted keys (K2b), free of the same-address
 // atomic contention (2.4k increments per bin at C2).
+// Each thread folds FOLD_PPT points (256-strided, coalesced): every point's
+// coordinate loads are issued before the first fold, so a warp keeps
+// FOLD_PPT x the bytes in flight (C2: one point per thread ran at ~2.5 TB/s,
+// latency bound).
+constexpr int FOLD_PPT = 4;
+
 template <typename TC, typename T>
 __global__ void __launch_bounds__(256)
 k_fold_keys(int M, const TC *__restrict__ x, const TC *__restrict__ y,
             const TC *__restrict__ z, int64_t stride, Geom g, int32_t *__restrict__ keys,
             int32_t *__restrict__ counts, unsigned long long *__restrict__ bad,
             int32_t *__restrict__ ckeys, int sb, T *__restrict__ rec) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    bool in = i < M;
-    unsigned mask = __ballot_sync(0xffffffffu, in);
-    if (!in) return;
+    const int i0 = blockIdx.x * (256 * FOLD_PPT) + threadIdx.x;
     const TC *ax[3] = {x, y, z};
-    int key = 0, kstride = 1;
-    int t[3] = {0, 0, 0}, pd[3] = {1, 1, 1};
-    T u[3] = {0, 0, 0};
-    bool ok = true;
+    double xin[FOLD_PPT][3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        if (a < g.dim) {
-            double xv = (double)ax[a][(int64_t)i * stride];
-            if (!isfinite(xv)) ok = false;
-            double v = ok ? nk_fold(xv, g.scale[a]) : 0.0;
-            int c = nk_cell(v, g.n[a]);
-            const int b = c / g.m[a];
-            key += kstride * b;
-            kstride *= g.nb[a];
-            // local coordinate in plan precision (K5: the visit-order
-            // gather copies these records) and, for SM plans, the footprint
-            // start in the bin's padded frame from the same value
-            const int corner = b * g.m[a];
-            u[a] = (T)(v - (double)corner);
-            if (ckeys) {
-                t[a] = (int)nk_ceil<T>(u[a] - (T)(0.5 * g.w)) + g.halo;
-                pd[a] = min(g.m[a], g.n[a] - corner) + 2 * g.halo;
+    for (int k = 0; k < FOLD_PPT; ++k)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int i = i0 + k * 256;
+            xin[k][a] = a < g.dim && i < M ? (double)ax[a][(int64_t)i * stride] : 0.0;
+        }
+#pragma unroll
+    for (int k = 0; k < FOLD_PPT; ++k) {
+        const int i = i0 + k * 256;
+        const bool in = i < M;
+        const unsigned mask = __ballot_sync(0xffffffffu, in);
+        if (!in) continue;   // every lane still reaches the next point's ballot
+        int key = 0, kstride = 1;
+        int t[3] = {0, 0, 0}, pd[3] = {1, 1, 1};
+        T u[3] = {0, 0, 0};
+        bool ok = true;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (a < g.dim) {
+                const double xv = xin[k][a];
+                if (!isfinite(xv)) ok = false;
+                double v = ok ? nk_fold(xv, g.scale[a]) : 0.0;
+                int c = nk_cell(v, g.n[a]);
+                const int b = c / g.m[a];
+                key += kstride * b;
+                kstride *= g.nb[a];
+                // local coordinate in plan precision (K5: the visit-order
+                // gather copies these records) and, for SM plans, the
+                // footprint start in the bin's padded frame from the same value
+                const int corner = b * g.m[a];
+                u[a] = (T)(v - (double)corner);
+                if (ckeys) {
+                    t[a] = (int)nk_ceil<T>(u[a] - (T)(0.5 * g.w)) + g.halo;
+                    pd[a] = min(g.m[a], g.n[a] - corner) + 2 * g.halo;
+                }
             }
         }
-    }
-    if (!ok) {
-        atomicMin(bad, (unsigned long long)i);
-        key = 0;
-        t[0] = t[1] = t[2] = 0;
-        u[0] = u[1] = u[2] = 0;
-    }
-    keys[i] = key;
-    // record (u1, u2[, u3, 0]): one aligned 8/16/32-byte vector per point
-    if (g.dim == 3) {
-        if constexpr (sizeof(T) == 8) {
-            double2 *r = reinterpret_cast<double2 *>(rec) + 2 * (int64_t)i;
-            r[0] = make_double2(u[0], u[1]);
-            r[1] = make_double2(u[2], 0.0);
-        } else {
-            reinterpret_cast<float4 *>(rec)[i] = make_float4(u[0], u[1], u[2], 0.0f);
+        if (!ok) {
+            atomicMin(bad, (unsigned long long)i);
+            key = 0;
+            t[0] = t[1] = t[2] = 0;
+            u[0] = u[1] = u[2] = 0;
         }
-    } else {
-        if constexpr (sizeof(T) == 8)
-            reinterpret_cast<double2 *>(rec)[i] = make_double2(u[0], u[1]);
-        else
-            reinterpret_cast<float2 *>(rec)[i] = make_float2(u[0], u[1]);
-    }
-    if (ckeys)
-        ckeys[i] = (int32_t)(((unsigned)key << sb) |
-                             (unsigned)nk_start_code(t[0], t[1], t[2], pd[0], pd[1], g));
-    if (counts) {
-        unsigned peers = __match_any_sync(mask, key);
-        if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&counts[key], __popc(peers));
+        keys[i] = key;
+        // record (u1, u2[, u3, 0]): one aligned 8/16/32-byte vector per point
+        if (g.dim == 3) {
+            if constexpr (sizeof(T) == 8) {
+                double2 *r = reinterpret_cast<double2 *>(rec) + 2 * (int64_t)i;
+                r[0] = make_double2(u[0], u[1]);
+                r[1] = make_double2(u[2], 0.0);
+            } else {
+                reinterpret_cast<float4 *>(rec)[i] = make_float4(u[0], u[1], u[2], 0.0f);
+            }
+        } else {
+            if constexpr (sizeof(T) == 8)
+                reinterpret_cast<double2 *>(rec)[i] = make_double2(u[0], u[1]);
+            else
+                reinterpret_cast<float2 *>(rec)[i] = make_float2(u[0], u[1]);
+        }
+        if (ckeys)
+            ckeys[i] = (int32_t)(((unsigned)key << sb) |
+                                 (unsigned)nk_start_code(t[0], t[1], t[2], pd[0], pd[1], g));
+        if (counts) {
+            unsigned peers = __match_any_sync(mask, key);
+            if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&counts[key], __popc(peers));
+        }
     }
 }
 
@@ -460,32 +478,52 @@ __global__ void k_det_keys(int S, const int32_t *__restrict__ sub_bin,
 // coordinates as one aligned record in input order; this gathers the
 // records through the visit permutation (one sector per point instead of
 // one per coordinate) and writes them as SoA rows.
+// FOLD_PPT points per thread, all permutation and record loads issued
+// before the first store (memory-level parallelism for the random reads).
+template <typename T, int D>
+__device__ __forceinline__ void load_rec(const T *__restrict__ rec, int64_t i, T *u) {
+    if constexpr (D == 3 && sizeof(T) == 8) {
+        const double2 a = __ldg(reinterpret_cast<const double2 *>(rec) + 2 * i);
+        u[0] = a.x;
+        u[1] = a.y;
+        u[2] = __ldg(rec + 4 * i + 2);
+    } else if constexpr (D == 3) {
+        const float4 a = __ldg(reinterpret_cast<const float4 *>(rec) + i);
+        u[0] = a.x;
+        u[1] = a.y;
+        u[2] = a.z;
+    } else if constexpr (sizeof(T) == 8) {
+        const double2 a = __ldg(reinterpret_cast<const double2 *>(rec) + i);
+        u[0] = a.x;
+        u[1] = a.y;
+    } else {
+        const float2 a = __ldg(reinterpret_cast<const float2 *>(rec) + i);
+        u[0] = a.x;
+        u[1] = a.y;
+    }
+}
+
 template <typename T, int D>
 __global__ void __launch_bounds__(256)
 k_gather_points(int M, const int32_t *__restrict__ perm, const T *__restrict__ rec,
                 T *__restrict__ pts, int64_t pitch) {
-    int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= M) return;
-    const int64_t i = perm ? perm[j] : j;
-    if constexpr (D == 3 && sizeof(T) == 8) {
-        const double2 a = __ldg(reinterpret_cast<const double2 *>(rec) + 2 * i);
-        const double b = __ldg(rec + 4 * i + 2);
-        pts[j] = a.x;
-        pts[pitch + j] = a.y;
-        pts[2 * pitch + j] = b;
-    } else if constexpr (D == 3) {
-        const float4 a = __ldg(reinterpret_cast<const float4 *>(rec) + i);
-        pts[j] = a.x;
-        pts[pitch + j] = a.y;
-        pts[2 * pitch + j] = a.z;
-    } else if constexpr (sizeof(T) == 8) {
-        const double2 a = __ldg(reinterpret_cast<const double2 *>(rec) + i);
-        pts[j] = a.x;
-        pts[pitch + j] = a.y;
-    } else {
-        const float2 a = __ldg(reinterpret_cast<const float2 *>(rec) + i);
-        pts[j] = a.x;
-        pts[pitch + j] = a.y;
+    const int j0 = blockIdx.x * (256 * FOLD_PPT) + threadIdx.x;
+    int src[FOLD_PPT];
+#pragma unroll
+    for (int k = 0; k < FOLD_PPT; ++k) {
+        const int j = j0 + k * 256;
+        src[k] = j < M ? (perm ? __ldcs(perm + j) : j) : -1;
+    }
+    T u[FOLD_PPT][D];
+#pragma unroll
+    for (int k = 0; k < FOLD_PPT; ++k)
+        if (src[k] >= 0) load_rec<T, D>(rec, src[k], u[k]);
+#pragma unroll
+    for (int k = 0; k < FOLD_PPT; ++k) {
+        const int j = j0 + k * 256;
+        if (src[k] < 0) continue;
+#pragma unroll
+        for (int a = 0; a < D; ++a) pts[a * pitch + j] = u[k][a];
     }
 }
 
@@ -680,11 +718,11 @@ static int fold_keys(nk_plan *p, const void *x, const void *y, const void *z, in
                      int32_t *ckeys, int sb) {
     int M = (int)p->M;
     if (p->prec == NK_DOUBLE)
-        k_fold_keys<TC, double><<<blocks_for(M, 256), 256, 0, p->stream>>>(
+        k_fold_keys<TC, double><<<blocks_for(M, 256 * FOLD_PPT), 256, 0, p->stream>>>(
             M, (const TC *)x, (const TC *)y, (const TC *)z, stride, p->geom, p->d_keys_in,
             p->method == NK_GM ? p->d_counts : nullptr, p->d_bad, ckeys, sb, (double *)p->d_rec);
     else
-        k_fold_keys<TC, float><<<blocks_for(M, 256), 256, 0, p->stream>>>(
+        k_fold_keys<TC, float><<<blocks_for(M, 256 * FOLD_PPT), 256, 0, p->stream>>>(
             M, (const TC *)x, (const TC *)y, (const TC *)z, stride, p->geom, p->d_keys_in,
             p->method == NK_GM ? p->d_counts : nullptr, p->d_bad, ckeys, sb, (float *)p->d_rec);
     NK_LAUNCH_CHECK();
@@ -695,10 +733,10 @@ template <typename T>
 static int gather(nk_plan *p, const int32_t *perm) {
     int M = (int)p->M;
     if (p->dim == 3)
-        k_gather_points<T, 3><<<blocks_for(M, 256), 256, 0, p->stream>>>(
+        k_gather_points<T, 3><<<blocks_for(M, 256 * FOLD_PPT), 256, 0, p->stream>>>(
             M, perm, (const T *)p->d_rec, (T *)p->d_pts, p->cap_M);
     else
-        k_gather_points<T, 2><<<blocks_for(M, 256), 256, 0, p->stream>>>(
+        k_gather_points<T, 2><<<blocks_for(M, 256 * FOLD_PPT), 256, 0, p->stream>>>(
             M, perm, (const T *)p->d_rec, (T *)p->d_pts, p->cap_M);
     NK_LAUNCH_CHECK();
     return NK_OK;

@@ -292,11 +292,27 @@ k_spread_sm3(const int32_t *__restrict__ sub_bin, const int32_t *__restrict__ su
 
 // Strengths in visit order for the tiled spread: cv[t][j] = c[t][perm[j]]
 // (one pass per execute; the spread then streams contiguous slices by TMA).
+// GV_PPT points per thread, every load issued before the first store
+// (memory-level parallelism for the random 16-byte reads).
+constexpr int GV_PPT = 4;
 __global__ void __launch_bounds__(256)
 k_gather_visit(int M, const int32_t *__restrict__ perm, const double2 *__restrict__ c,
                int64_t cpitch, double2 *__restrict__ cv, int64_t vpitch) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < M) cv[blockIdx.y * vpitch + j] = c[blockIdx.y * cpitch + perm[j]];
+    const int j0 = blockIdx.x * (256 * GV_PPT) + threadIdx.x;
+    c += blockIdx.y * cpitch;
+    cv += blockIdx.y * vpitch;
+    int src[GV_PPT];
+#pragma unroll
+    for (int k = 0; k < GV_PPT; ++k) {
+        const int j = j0 + k * 256;
+        src[k] = j < M ? __ldg(perm + j) : -1;
+    }
+    double2 v[GV_PPT];
+#pragma unroll
+    for (int k = 0; k < GV_PPT; ++k) v[k] = src[k] >= 0 ? __ldg(c + src[k]) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < GV_PPT; ++k)
+        if (src[k] >= 0) cv[j0 + k * 256] = v[k];
 }
 inline int64_t g_M(const nk_plan *p) { return p->M; }
 
@@ -791,7 +807,8 @@ int launch_w(nk_plan *p, const void *c, void *fine, int *launches) {
                 NK_CUDA(cudaMalloc(&p->d_cvis, 16 * (size_t)need));
                 p->cap_cvis = need;
             }
-            k_gather_visit<<<dim3((M + 255) / 256, p->ntrans), 256, 0, p->stream>>>(
+            k_gather_visit<<<dim3((M + 256 * GV_PPT - 1) / (256 * GV_PPT), p->ntrans), 256, 0,
+                             p->stream>>>(
                 M, p->d_vperm, (const double2 *)c, g_M(p), (double2 *)p->d_cvis, p->cap_M);
             NK_LAUNCH_CHECK();
             ++*launches;

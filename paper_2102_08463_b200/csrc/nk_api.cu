@@ -70,6 +70,7 @@ void free_plan(nk_plan *p) {
     for (void *b : bufs)
         if (b) cudaFree(b);
     free(p->h_det_off);
+    if (p->h_flags) cudaFreeHost(p->h_flags);
     if (p->fft_ok) cufftDestroy(p->fft);
     if (p->fft_col_ok) cufftDestroy(p->fft_col);
     if (p->d_twiddle) cudaFree(p->d_twiddle);
@@ -417,7 +418,14 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
     NK_ALLOC(p->d_counts, 4 * p->nbins);
     NK_ALLOC(p->d_starts, 4 * (p->nbins + 1));
     NK_ALLOC(p->d_nsub_off, 4 * (p->nbins + 1));
-    NK_ALLOC(p->d_bad, sizeof(unsigned long long));
+    NK_ALLOC(p->d_bad, 4 * sizeof(unsigned long long));
+    e = cudaMallocHost((void **)&p->h_flags, 4 * sizeof(unsigned long long));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        p->h_flags = nullptr;
+        nk_set_error(std::string("pinned host allocation failed: ") + cudaGetErrorString(e));
+        return fail(NK_ERR_MEMORY);
+    }
     NK_ALLOC(p->d_work, sizeof(int) * p->ntrans);
 #undef NK_ALLOC
     if (precision == NK_DOUBLE) {

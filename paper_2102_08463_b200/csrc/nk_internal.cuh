@@ -119,7 +119,8 @@ struct nk_plan {
     int64_t cap_tile_hist;
     int32_t *d_scan_tmp;
     int64_t cap_scan_tmp;
-    unsigned long long *d_bad;
+    unsigned long long *d_bad;    // [0] first non-finite index, [1] sum count^2, [2] S
+    unsigned long long *h_flags;  // pinned copy of d_bad[0..2]: setpts' one host sync
     bool sorted;
     bool perm_valid;        // d_perm holds the bin-stable layout (else derived on demand)
 

@@ -835,19 +835,17 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
     int32_t *ck = composite ? p->d_sort_scr : nullptr;
     NK_CUDA(cudaMemsetAsync(p->d_counts, 0, sizeof(int32_t) * nbins, st));
     NK_CUDA(cudaMemsetAsync(p->d_bad, 0xff, sizeof(unsigned long long), st));
+    NK_CUDA(cudaMemsetAsync(p->d_bad + 1, 0, 2 * sizeof(unsigned long long), st));
     if (M > 0) {
         rc = coord_prec == NK_DOUBLE ? fold_keys<double>(p, x, y, z, stride, ck, sb)
                                      : fold_keys<float>(p, x, y, z, stride, ck, sb);
         if (rc) return rc;
     }
-    unsigned long long bad = ~0ull;
-    NK_CUDA(cudaMemcpyAsync(&bad, p->d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
-    NK_CUDA(cudaStreamSynchronize(st));
-    if (bad != ~0ull) {
-        nk_set_error_index((int64_t)bad);
-        nk_set_error("non-finite coordinate at point index " + std::to_string(bad));
-        return NK_ERR_NONFINITE;
-    }
+    // The non-finite check is read back together with the subproblem count
+    // (and the bin-density sum of the type-2 visit-order choice) in setpts'
+    // single host synchronisation below: a non-finite point folds to key 0 /
+    // coordinate 0, so the sort in between is harmless, and have_points stays
+    // false on the error return.
     const int32_t *perm = nullptr;
     p->sorted = false;
     p->perm_valid = false;
@@ -886,15 +884,37 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
     // subproblems (binsort.py:166-219), needed by the SM spread and the
     // staged interpolation
     p->S = 0;
+    // type-2 SM plans with a composite key and the per-thread gather choose
+    // their visit order from the point-weighted bin density (below)
+    const bool xwin = nk_interp_xwin(p->type, p->dim, p->prec, p->w, p->method,
+                                     p->max_sub_smem) ||
+                      p->geom.tiled;
+    const bool need_sq = p->method == NK_SM && p->type == 2 && composite && !xwin && M > 0;
     if (p->method == NK_SM && M > 0) {
         k_nsub<<<blocks_for(nbins, 256), 256, 0, st>>>(p->d_counts, nbins, p->msub,
                                                        p->d_nsub_off);
         NK_LAUNCH_CHECK();
         rc = nk_scan_exclusive(p, p->d_nsub_off, p->d_nsub_off, nbins);
         if (rc) return rc;
-        int32_t S = 0;
-        NK_CUDA(cudaMemcpyAsync(&S, p->d_nsub_off + nbins, 4, cudaMemcpyDeviceToHost, st));
-        NK_CUDA(cudaStreamSynchronize(st));
+        NK_CUDA(cudaMemcpyAsync(p->d_bad + 2, p->d_nsub_off + nbins, 4,
+                                cudaMemcpyDeviceToDevice, st));
+    }
+    if (need_sq) {
+        k_sum_sq<<<std::min(blocks_for(nbins, 256), 1184u), 256, 0, st>>>(nbins, p->d_counts,
+                                                                         p->d_bad + 1);
+        NK_LAUNCH_CHECK();
+    }
+    NK_CUDA(cudaMemcpyAsync(p->h_flags, p->d_bad, 3 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));
+    NK_CUDA(cudaStreamSynchronize(st));
+    const unsigned long long bad = p->h_flags[0];
+    if (bad != ~0ull) {
+        nk_set_error_index((int64_t)bad);
+        nk_set_error("non-finite coordinate at point index " + std::to_string(bad));
+        return NK_ERR_NONFINITE;
+    }
+    if (p->method == NK_SM && M > 0) {
+        const int32_t S = (int32_t)p->h_flags[2];
         p->S = S;
         if (S > 0) {
             if (S > p->cap_S || !p->d_sub_bin) {
@@ -929,9 +949,6 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
             if (rc) return rc;
         } else if (p->type == 2) {
             // K7x / K7t group neighbours in footprint-start order
-            const bool xwin = nk_interp_xwin(p->type, p->dim, p->prec, p->w, p->method,
-                                             p->max_sub_smem) ||
-                              p->geom.tiled;
             bool interleave = !composite && p->prec == NK_DOUBLE && !xwin;
             if (xwin) {
                 // K7x groups neighbours in footprint-start order
@@ -940,14 +957,7 @@ int nk_sort_points(nk_plan *p, int coord_prec, const void *x, const void *y, con
                     if (rc) return rc;
                 }
             } else if (composite) {
-                unsigned long long *d_sq = p->d_bad;   // reused: setpts' error flag is read
-                NK_CUDA(cudaMemsetAsync(d_sq, 0, sizeof(unsigned long long), st));
-                k_sum_sq<<<std::min(blocks_for(nbins, 256), 1184u), 256, 0, st>>>(
-                    nbins, p->d_counts, d_sq);
-                NK_LAUNCH_CHECK();
-                unsigned long long sq = 0;
-                NK_CUDA(cudaMemcpyAsync(&sq, d_sq, sizeof(sq), cudaMemcpyDeviceToHost, st));
-                NK_CUDA(cudaStreamSynchronize(st));
+                const unsigned long long sq = p->h_flags[1];   // need_sq: read back above
                 double cells = 1;
                 for (int i = 0; i < p->dim; ++i) cells *= p->bin_dims[i];
                 const double rho = (double)sq / ((double)M * cells);

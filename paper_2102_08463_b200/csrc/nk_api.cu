@@ -334,6 +334,12 @@ extern "C" int nk_plan_create(int type, int dim, const int64_t *modes, double ep
         g.N[i] = (int)p->N[i];
         g.m[i] = p->bin_dims[i];
         g.nb[i] = (int)p->nb[i];
+        // multiply-high division of a cell index by the bin width (K1): exact
+        // when cell * m < 2^32 for every cell < n (floor(c ceil(2^32/m) / 2^32)
+        // = floor(c / m) while c m <= 2^32)
+        g.mdiv[i] = g.m[i] > 1 && (uint64_t)p->n[i] * (uint64_t)g.m[i] <= (1ull << 32)
+                        ? (unsigned)(((1ull << 32) + g.m[i] - 1) / g.m[i])
+                        : 0u;
         g.scale[i] = (double)p->n[i] / NK_TWO_PI;   // binsort.py:99
     }
     g.halo = p->halo;

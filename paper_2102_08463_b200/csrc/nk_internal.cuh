@@ -38,6 +38,7 @@ struct Geom {
     int N[3];       // mode counts
     int m[3];       // bin dims
     int nb[3];      // bins per axis
+    unsigned mdiv[3];  // ceil(2^32 / m): cell / m = umulhi(cell, mdiv) (exact: n m <= 2^32), 0 = divide
     int halo;       // ceil(w/2)
     int w;
     // footprint-start visit code (setpts K4d): 0 = lexicographic

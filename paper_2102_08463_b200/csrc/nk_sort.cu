@@ -46,6 +46,7 @@ k_fold_keys(int M, const TC *__restrict__ x, const TC *__restrict__ y,
             int32_t *__restrict__ ckeys, int sb, T *__restrict__ rec) {
     const int i0 = blockIdx.x * (256 * FOLD_PPT) + threadIdx.x;
     const TC *ax[3] = {x, y, z};
+    const T halfw = (T)(0.5 * g.w);
     double xin[FOLD_PPT][3];
 #pragma unroll
     for (int k = 0; k < FOLD_PPT; ++k)
@@ -70,8 +71,10 @@ k_fold_keys(int M, const TC *__restrict__ x, const TC *__restrict__ y,
                 const double xv = xin[k][a];
                 if (!isfinite(xv)) ok = false;
                 double v = ok ? nk_fold(xv, g.scale[a]) : 0.0;
-                int c = nk_cell(v, g.n[a]);
-                const int b = c / g.m[a];
+                // cell = clamp(floor(v), 0, n - 1) (nk_cell; v is finite and in
+                // [0, n] here) with one conversion; bin by multiply-high
+                const int c = min(max(__double2int_rd(v), 0), g.n[a] - 1);
+                const int b = g.mdiv[a] ? (int)__umulhi((unsigned)c, g.mdiv[a]) : c / g.m[a];
                 key += kstride * b;
                 kstride *= g.nb[a];
                 // local coordinate in plan precision (K5: the visit-order
@@ -80,7 +83,7 @@ k_fold_keys(int M, const TC *__restrict__ x, const TC *__restrict__ y,
                 const int corner = b * g.m[a];
                 u[a] = (T)(v - (double)corner);
                 if (ckeys) {
-                    t[a] = (int)nk_ceil<T>(u[a] - (T)(0.5 * g.w)) + g.halo;
+                    t[a] = (int)nk_ceil<T>(u[a] - halfw) + g.halo;
                     pd[a] = min(g.m[a], g.n[a] - corner) + 2 * g.halo;
                 }
             }

@@ -260,7 +260,7 @@ k_scan_down(const int32_t *in, int64_t n, const int32_t *__restrict__ partials,
 // (warp-striped order, __match_any_sync peers + per-warp digit counters)
 // and scatters (key, value) to its global slot.
 __global__ void __launch_bounds__(SORT_BLOCK)
-k_radix_hist(const int32_t *__restrict__ keys, int M, int shift, int ntiles,
+k_radix_hist(const int32_t *__restrict__ keys, int M, int shift, int dmask, int ntiles,
              int32_t *__restrict__ hist) {
     // per-warp digit histograms with native shared integer atomics (no
     // match.any: ranks are not needed here), 16-byte key loads
@@ -274,14 +274,14 @@ k_radix_hist(const int32_t *__restrict__ keys, int M, int shift, int ntiles,
 #pragma unroll
         for (int v = 0; v < SORT_ITEMS / 4; ++v) {
             const int4 q = __ldg(k4 + v);
-            atomicAdd(&h[warp][(q.x >> shift) & (RADIX - 1)], 1);
-            atomicAdd(&h[warp][(q.y >> shift) & (RADIX - 1)], 1);
-            atomicAdd(&h[warp][(q.z >> shift) & (RADIX - 1)], 1);
-            atomicAdd(&h[warp][(q.w >> shift) & (RADIX - 1)], 1);
+            atomicAdd(&h[warp][(q.x >> shift) & dmask], 1);
+            atomicAdd(&h[warp][(q.y >> shift) & dmask], 1);
+            atomicAdd(&h[warp][(q.z >> shift) & dmask], 1);
+            atomicAdd(&h[warp][(q.w >> shift) & dmask], 1);
         }
     } else {
         for (int it = 0; it < SORT_ITEMS; ++it)
-            if (base + it < M) atomicAdd(&h[warp][(keys[base + it] >> shift) & (RADIX - 1)], 1);
+            if (base + it < M) atomicAdd(&h[warp][(keys[base + it] >> shift) & dmask], 1);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < RADIX; i += blockDim.x) {
@@ -292,6 +292,7 @@ k_radix_hist(const int32_t *__restrict__ keys, int M, int shift, int ntiles,
     }
 }
 
+template <int DB>
 __global__ void __launch_bounds__(SORT_BLOCK)
 k_radix_scatter(const int32_t *__restrict__ keys_in, const int32_t *__restrict__ vals_in,
                 int M, int shift, int ntiles, const int32_t *__restrict__ offs,
@@ -310,6 +311,7 @@ k_radix_scatter(const int32_t *__restrict__ keys_in, const int32_t *__restrict__
     const int tbase = blockIdx.x * SORT_TILE;
     const int base = tbase + warp * 32 * SORT_ITEMS;
     const unsigned lt = (1u << lane) - 1u;
+    constexpr int dmask = (1 << DB) - 1;
     int key[SORT_ITEMS], val[SORT_ITEMS], rank[SORT_ITEMS];
     // all of the warp's loads in flight before the ranking (the ranking's
     // ballots / shuffles would otherwise wait on each load in turn)
@@ -323,10 +325,10 @@ k_radix_scatter(const int32_t *__restrict__ keys_in, const int32_t *__restrict__
     for (int it = 0; it < SORT_ITEMS; ++it) {
         int idx = base + it * 32 + lane;
         bool valid = idx < M;
-        const int d = (key[it] >> shift) & (RADIX - 1);
+        const int d = (key[it] >> shift) & dmask;
         unsigned peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
-        for (int b = 0; b < RADIX_BITS; ++b) {
+        for (int b = 0; b < DB; ++b) {
             const unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1);
             peers &= ((d >> b) & 1) ? bb : ~bb;
         }
@@ -361,7 +363,7 @@ k_radix_scatter(const int32_t *__restrict__ keys_in, const int32_t *__restrict__
 #pragma unroll
     for (int it = 0; it < SORT_ITEMS; ++it) {
         if (rank[it] >= 0) {
-            const int d = (key[it] >> shift) & (RADIX - 1);
+            const int d = (key[it] >> shift) & dmask;
             const int lp = lstart[d] + wcnt[warp][d] + rank[it];
             skey[lp] = key[it];
             sval[lp] = val[it];
@@ -371,7 +373,7 @@ k_radix_scatter(const int32_t *__restrict__ keys_in, const int32_t *__restrict__
     const int n = min(SORT_TILE, M - tbase);
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
         const int k = skey[t];
-        const int d = (k >> shift) & (RADIX - 1);
+        const int d = (k >> shift) & dmask;
         const int pos = gstart[d] + (t - lstart[d]);
         keys_out[pos] = k;
         vals_out[pos] = sval[t];
@@ -754,6 +756,9 @@ static int radix_sort_pairs(nk_plan *p, const int32_t *kin, const int32_t *vin, 
                             int32_t *tmp_v) {
     cudaStream_t st = p->stream;
     const int passes = std::max(1, (bits + RADIX_BITS - 1) / RADIX_BITS);
+    // the bits spread evenly over the passes (C4's 28-bit key: 4 x 7 rather
+    // than 8 + 8 + 8 + 4): fewer ranking ballots per pass, longer digit runs
+    const int dbits = std::min(RADIX_BITS, std::max(4, (bits + passes - 1) / passes));
     const int ntiles = (int)((M + SORT_TILE - 1) / SORT_TILE);
     int rc = grow(&p->d_tile_hist, &p->cap_tile_hist, (int64_t)RADIX * ntiles + 1);
     if (rc) return rc;
@@ -761,13 +766,19 @@ static int radix_sort_pairs(nk_plan *p, const int32_t *kin, const int32_t *vin, 
     for (int ps = 0; ps < passes; ++ps) {
         const bool toA = ((passes - 1 - ps) % 2) == 0;   // the last pass lands in A
         int32_t **dst = toA ? A : B;
-        const int shift = ps * RADIX_BITS;
-        k_radix_hist<<<ntiles, SORT_BLOCK, 0, st>>>(kin, (int)M, shift, ntiles, p->d_tile_hist);
+        const int shift = ps * dbits;
+        k_radix_hist<<<ntiles, SORT_BLOCK, 0, st>>>(kin, (int)M, shift, (1 << dbits) - 1, ntiles,
+                                                    p->d_tile_hist);
         NK_LAUNCH_CHECK();
         rc = nk_scan_exclusive(p, p->d_tile_hist, p->d_tile_hist, (int64_t)RADIX * ntiles);
         if (rc) return rc;
-        k_radix_scatter<<<ntiles, SORT_BLOCK, 0, st>>>(kin, vin, (int)M, shift, ntiles,
-                                                       p->d_tile_hist, dst[0], dst[1]);
+        auto kern = dbits >= 8 ? k_radix_scatter<8>
+                  : dbits == 7 ? k_radix_scatter<7>
+                  : dbits == 6 ? k_radix_scatter<6>
+                  : dbits == 5 ? k_radix_scatter<5>
+                  : k_radix_scatter<4>;
+        kern<<<ntiles, SORT_BLOCK, 0, st>>>(kin, vin, (int)M, shift, ntiles, p->d_tile_hist,
+                                            dst[0], dst[1]);
         NK_LAUNCH_CHECK();
         kin = dst[0];
         vin = dst[1];

@@ -145,7 +145,11 @@ NK_API int nk_set_stream(nk_plan *plan, void *stream);
  * set_pts(X, Y, Z); stride d = the reference's (M, d) array).  coord_prec
  * is NK_SINGLE or NK_DOUBLE (coordinates are widened to FP64 for the fold,
  * binsort.py:123).  Non-finite coordinates -> NK_ERR_NONFINITE naming the
- * first offending index.  M = 0 is legal. */
+ * first offending index.  M = 0 is legal.  Unlike nk_execute, setpts always
+ * waits for the plan stream before returning: the subproblem count sizes
+ * host-side launches, so it reads that count back together with the
+ * non-finite check (one synchronisation; the deterministic option adds its
+ * colour-class readback). */
 NK_API int nk_setpts(nk_plan *plan, int64_t M, int coord_prec, const void *x, const void *y,
               const void *z, int64_t stride);
 
